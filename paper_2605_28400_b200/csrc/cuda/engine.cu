@@ -1,0 +1,861 @@
+// engine.cu — host engine + C-ABI (include/trioalign_capi.h).
+//
+// Replaces the reference batch path: plan_partition/run_batch/run_worker
+// (/root/reference/proj/src/dispatch.cpp:29-162) and the engine entry points
+// align / oracle_align (tiled.cpp:62-71, oracle.cpp:182-190).  One call:
+//   host ASCII -> H2D -> 2-bit pack (device) -> length buckets -> persistent
+//   wavefront kernels (K1, or K2 + K3 walker for rows) -> D2H results.
+// There is no CPU fallback: every alignment is computed by the kernels in
+// wavefront.cuh; a missing/failed device is reported as TA_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../../include/trioalign_capi.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define TA_CK(expr)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess) return fail(TA_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device buffers
+
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;  // elements
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+  }
+  cudaError_t reserve(size_t n) {
+    if (n <= cap && ptr) return cudaSuccess;
+    release();
+    const size_t want = std::max<size_t>(n, 1);
+    cudaError_t e = cudaMalloc(&ptr, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// kernels around the wavefront
+
+// One warp per sequence: ASCII -> 2-bit codes, 16 bases per word.
+__global__ void pack_kernel(const char* __restrict__ ascii, const int64_t* __restrict__ src_off,
+                            const int32_t* __restrict__ len, const uint32_t* __restrict__ dst_word,
+                            int64_t nseq, uint32_t* __restrict__ seq, int32_t* __restrict__ bad) {
+  const int64_t s = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (s >= nseq) return;
+  const char* src = ascii + src_off[s];
+  const int L = len[s];
+  const int nw = (L + 15) >> 4;
+  bool badc = false;
+  for (int w = lane; w < nw; w += 32) {
+    uint32_t word = 0;
+    const int base = w * 16;
+    const int cnt = min(16, L - base);
+    for (int q = 0; q < cnt; ++q) {
+      const char ch = src[base + q];
+      uint32_t code;
+      switch (ch) {
+        case 'A': code = 0; break;
+        case 'C': code = 1; break;
+        case 'G': code = 2; break;
+        case 'T': code = 3; break;
+        default: code = 0; badc = true; break;
+      }
+      word |= code << (2 * q);
+    }
+    seq[dst_word[s] + w] = word;
+  }
+  if (__any_sync(0xFFFFFFFFu, badc) && lane == 0) bad[s / 3] = 1;
+}
+
+// (value, lexicographic index) keys -> score and end coordinates.
+__global__ void decode_keys_kernel(const unsigned long long* __restrict__ key,
+                                   const ta::TripletDesc* __restrict__ desc,
+                                   const int32_t* __restrict__ ids, int64_t n,
+                                   int32_t* __restrict__ score, int32_t* __restrict__ end) {
+  const int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int32_t id = ids[x];
+  const unsigned long long k = key[id];
+  const ta::TripletDesc d = desc[id];
+  const uint32_t lin = 0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFull);
+  const uint32_t plane = static_cast<uint32_t>(d.b + 1) * static_cast<uint32_t>(d.c + 1);
+  const uint32_t i = lin / plane;
+  const uint32_t rem = lin - i * plane;
+  const uint32_t j = rem / static_cast<uint32_t>(d.c + 1);
+  const uint32_t kk = rem - j * static_cast<uint32_t>(d.c + 1);
+  score[id] = static_cast<int32_t>(static_cast<uint32_t>(k >> 32) ^ 0x80000000u);
+  end[3 * id] = static_cast<int32_t>(i);
+  end[3 * id + 1] = static_cast<int32_t>(j);
+  end[3 * id + 2] = static_cast<int32_t>(kk);
+}
+
+__device__ __forceinline__ char base_char(const uint32_t* seq, uint32_t w, int pos) {
+  const uint32_t code = (seq[w + (pos >> 4)] >> ((pos & 15) * 2)) & 3u;
+  return "ACGT"[code];
+}
+
+// K3: traceback walker over the direction cube (oracle.cpp:98-180).  One
+// thread per triplet: walk from `end` choosing the recorded first-max term;
+// stop at (0,0,0) (global), an axis cell (semi) or a floor cell (local);
+// emit rows with semi-global free prefix / suffix columns.
+__global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
+                              const uint32_t* __restrict__ seq, const int32_t* __restrict__ ids,
+                              int n, const uint32_t* __restrict__ dirs,
+                              const int64_t* __restrict__ dir_off, int grid, int mode,
+                              const int32_t* __restrict__ end, int32_t* __restrict__ begin,
+                              char* __restrict__ rows, const int64_t* __restrict__ row_off,
+                              int32_t* __restrict__ row_len, int32_t* __restrict__ status) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int id = ids[x];
+  const ta::TripletDesc d = desc[id];
+  constexpr int N = ta::kTileN;
+  const int T = grid * grid;
+  const uint32_t* base = dirs + dir_off[id] * 4;
+  auto code_at = [&](int i, int j, int k) -> uint32_t {
+    const int t = (j / N) * grid + (k / N);
+    const int cell = (j % N) * N + (k % N);
+    const uint32_t w = base[(int64_t(i) * T + t) * 16 + (cell >> 3)];
+    return (w >> ((cell & 7) * 4)) & 15u;
+  };
+  auto stop_at = [&](int i, int j, int k, uint32_t code) {
+    if (mode == ta::kGlobal) return i == 0 && j == 0 && k == 0;
+    if (mode == ta::kSemi) return (j == 0 && k == 0) || (i == 0 && k == 0) || (i == 0 && j == 0);
+    return code == ta::kTagStop;
+  };
+  const int ei = end[3 * id], ej = end[3 * id + 1], ek = end[3 * id + 2];
+  // pass 1: path length and begin
+  int i = ei, j = ej, k = ek, steps = 0;
+  const int limit = d.a + d.b + d.c + 1;
+  bool ok = true;
+  for (;;) {
+    const uint32_t code = (mode == ta::kLocal) ? code_at(i, j, k) : 0u;
+    if (stop_at(i, j, k, code)) break;
+    const uint32_t c = (mode == ta::kLocal) ? code : code_at(i, j, k);
+    int di, dj, dk;
+    switch (c) {
+      case ta::kTagT1: di = 1, dj = 1, dk = 1; break;
+      case ta::kTagT2: di = 1, dj = 1, dk = 0; break;
+      case ta::kTagT3: di = 1, dj = 0, dk = 1; break;
+      case ta::kTagT4: di = 0, dj = 1, dk = 1; break;
+      case ta::kTagT5: di = 1, dj = 0, dk = 0; break;
+      case ta::kTagT6: di = 0, dj = 1, dk = 0; break;
+      case ta::kTagT7: di = 0, dj = 0, dk = 1; break;
+      default: di = dj = dk = -1; break;
+    }
+    if (di < 0 || i - di < 0 || j - dj < 0 || k - dk < 0 || ++steps > limit) {
+      ok = false;
+      break;
+    }
+    i -= di, j -= dj, k -= dk;
+  }
+  if (!ok) {
+    status[id] = TA_ERR_LOGIC;
+    row_len[id] = 0;
+    return;
+  }
+  begin[3 * id] = i, begin[3 * id + 1] = j, begin[3 * id + 2] = k;
+  const int bi = i, bj = j, bk = k;
+  const bool semi = mode == ta::kSemi;
+  const int prefix = semi ? (bi + bj + bk) : 0;
+  const int suffix = semi ? ((d.a - ei) + (d.b - ej) + (d.c - ek)) : 0;
+  const int len = prefix + steps + suffix;
+  row_len[id] = len;
+  const int64_t cap = int64_t(d.a) + d.b + d.c;
+  char* r0 = rows + row_off[id];
+  char* r1 = r0 + cap;
+  char* r2 = r1 + cap;
+  int pos = 0;
+  if (semi) {
+    for (int p = 0; p < bi; ++p, ++pos) r0[pos] = base_char(seq, d.w0, p), r1[pos] = '-', r2[pos] = '-';
+    for (int p = 0; p < bj; ++p, ++pos) r0[pos] = '-', r1[pos] = base_char(seq, d.w1, p), r2[pos] = '-';
+    for (int p = 0; p < bk; ++p, ++pos) r0[pos] = '-', r1[pos] = '-', r2[pos] = base_char(seq, d.w2, p);
+  }
+  // pass 2: write the path columns back to front
+  i = ei, j = ej, k = ek;
+  for (int s = steps - 1; s >= 0; --s) {
+    const uint32_t c = code_at(i, j, k);
+    const int at = prefix + s;
+    const bool u0 = c == ta::kTagT1 || c == ta::kTagT2 || c == ta::kTagT3 || c == ta::kTagT5;
+    const bool u1 = c == ta::kTagT1 || c == ta::kTagT2 || c == ta::kTagT4 || c == ta::kTagT6;
+    const bool u2 = c == ta::kTagT1 || c == ta::kTagT3 || c == ta::kTagT4 || c == ta::kTagT7;
+    r0[at] = u0 ? base_char(seq, d.w0, i - 1) : '-';
+    r1[at] = u1 ? base_char(seq, d.w1, j - 1) : '-';
+    r2[at] = u2 ? base_char(seq, d.w2, k - 1) : '-';
+    i -= u0, j -= u1, k -= u2;
+  }
+  pos = prefix + steps;
+  if (semi) {
+    for (int p = ei; p < d.a; ++p, ++pos) r0[pos] = base_char(seq, d.w0, p), r1[pos] = '-', r2[pos] = '-';
+    for (int p = ej; p < d.b; ++p, ++pos) r0[pos] = '-', r1[pos] = base_char(seq, d.w1, p), r2[pos] = '-';
+    for (int p = ek; p < d.c; ++p, ++pos) r0[pos] = '-', r1[pos] = '-', r2[pos] = base_char(seq, d.w2, p);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-device context (stream + events), created lazily
+
+struct DeviceCtx {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int sms = 0;
+};
+
+std::mutex g_ctx_mu;
+std::vector<std::unique_ptr<DeviceCtx>> g_ctx;
+
+int get_ctx(int device, DeviceCtx** out) {
+  std::lock_guard<std::mutex> lock(g_ctx_mu);
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    return fail(TA_ERR_CUDA, std::string("no CUDA device available: ") +
+                                 (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                                 " (the trioalign B200 engine has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) return fail(TA_ERR_CUDA, "device index out of range");
+  if (g_ctx.size() < size_t(count)) g_ctx.resize(size_t(count));
+  if (!g_ctx[device]) {
+    auto ctx = std::make_unique<DeviceCtx>();
+    ctx->device = device;
+    TA_CK(cudaSetDevice(device));
+    TA_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    TA_CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
+    g_ctx[device] = std::move(ctx);
+  }
+  TA_CK(cudaSetDevice(device));
+  *out = g_ctx[device].get();
+  return TA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// scheme / option validation with reference semantics
+
+int validate_scheme(const ta_scheme& s) {
+  // core.cpp:10-18
+  if (s.match <= 0) return fail(TA_ERR_INVALID_ARGUMENT, "match score must be positive");
+  if (s.mismatch > 0) return fail(TA_ERR_INVALID_ARGUMENT, "mismatch score must be <= 0");
+  if (s.gap > 0) return fail(TA_ERR_INVALID_ARGUMENT, "gap score must be <= 0");
+  if (std::abs(s.match) > 1024 || std::abs(s.mismatch) > 1024 || std::abs(s.gap) > 1024)
+    return fail(TA_ERR_INVALID_ARGUMENT, "score magnitudes must be <= 1024");
+  return TA_OK;
+}
+
+int validate_options(const ta_options& o) {
+  // tiled.cpp:8-15
+  if (o.tile_size < 1 || o.tile_size > 4096)
+    return fail(TA_ERR_CONFIG, "tile size must be in [1, 4096], got " + std::to_string(o.tile_size));
+  if (o.team_width < 0) return fail(TA_ERR_CONFIG, "team width must be >= 0");
+  if (o.team_threads < 1) return fail(TA_ERR_CONFIG, "team threads must be >= 1");
+  if (o.cell_budget == 0) return fail(TA_ERR_CONFIG, "cell budget must be positive");
+  if (o.mode < 0 || o.mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "unknown alignment mode");
+  return TA_OK;
+}
+
+int32_t derive_team_width(int32_t tile_size, int32_t b, int32_t c) {
+  const int32_t need = std::max(b, c);
+  if (need <= 0) return 1;
+  return (need + tile_size - 1) / tile_size;
+}
+
+// ---------------------------------------------------------------------------
+// lane choice: s16x2 is used only when every value provably fits (exact)
+
+struct LanePlan {
+  bool packed16 = false;
+};
+
+bool s16_ok(const ta_scheme& s, int max_a, int grid) {
+  const int g2 = 2 * s.gap;
+  const int mp = s.match - g2, mm = s.mismatch - g2;
+  if (mm < 0 || mp > 127) return false;  // carry-free IADD3 + byte tables
+  const int64_t ext = int64_t(grid) * ta::kTileN;
+  const int64_t bound = int64_t(s.match - g2) * (int64_t(max_a) + 2 * ext) + 3 * 127 +
+                        int64_t(-g2) * 2 * ta::kTileN;
+  return bound <= 16000;
+}
+
+int pick_grid(int32_t b, int32_t c) {
+  const int ext = std::max(b, c) + 1;
+  for (int g : ta::kGridSizes)
+    if (g * ta::kTileN >= ext) return g;
+  return -1;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// the batch object
+
+struct ta_batch {
+  int device = 0;
+  DeviceCtx* ctx = nullptr;
+  int64_t n = 0;
+  std::vector<int32_t> a, b, c;
+  std::vector<ta::TripletDesc> desc;
+  std::vector<int32_t> pre_status;   // parse errors
+  std::vector<int32_t> status;       // last run
+  DevBuf<uint32_t> seq;
+  DevBuf<ta::TripletDesc> d_desc;
+  DevBuf<int32_t> d_score, d_end, d_begin, d_status, d_rowlen;
+  DevBuf<unsigned long long> d_key;
+  DevBuf<int32_t> d_items, d_soff, d_steps, d_ids;
+  DevBuf<uint4> d_dirs;
+  DevBuf<int64_t> d_diroff, d_rowoff;
+  DevBuf<char> d_rows;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  ta_stats stats{};
+  int last_mode = -1;
+  bool last_rows = false;
+  ~ta_batch() {
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+  }
+};
+
+namespace {
+
+struct StreamPlan {
+  std::vector<int32_t> items, soff, steps;
+};
+
+// Greedy least-loaded assignment of triplets to CTA lane streams (the
+// "dynamic" rule of plan_partition, dispatch.cpp:46-56, applied to slices).
+void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, int ctas,
+                  int lanes, int grid, StreamPlan* out) {
+  const int S = ctas * lanes;
+  std::vector<std::vector<int32_t>> lists(static_cast<size_t>(S));
+  using Load = std::pair<int64_t, int32_t>;
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int s = 0; s < S; ++s) heap.push({0, s});
+  std::vector<int64_t> load(size_t(S), 0);
+  for (int32_t id : ids) {
+    Load top = heap.top();
+    heap.pop();
+    lists[size_t(top.second)].push_back(id);
+    top.first += a[size_t(id)] + 1;
+    load[size_t(top.second)] = top.first;
+    heap.push(top);
+  }
+  out->items.clear();
+  out->soff.assign(size_t(S) + 1, 0);
+  out->steps.assign(size_t(ctas), 0);
+  for (int s = 0; s < S; ++s) {
+    out->soff[size_t(s)] = int32_t(out->items.size());
+    out->items.insert(out->items.end(), lists[size_t(s)].begin(), lists[size_t(s)].end());
+  }
+  out->soff[size_t(S)] = int32_t(out->items.size());
+  for (int cta = 0; cta < ctas; ++cta) {
+    int64_t mx = 0;
+    for (int l = 0; l < lanes; ++l) mx = std::max(mx, load[size_t(cta * lanes + l)]);
+    out->steps[size_t(cta)] = int32_t(mx + 2 * (grid - 1));
+  }
+}
+
+struct BucketLaunch {
+  ta::KernelEntry ke;
+  int ctas = 0;
+  DevBuf<int32_t> items, soff, steps;
+  int64_t padded = 0;
+};
+
+// Host planning + upload for one bucket (outside any timed region).
+int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
+                   bool trace, cudaStream_t st, BucketLaunch* bl) {
+  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace);
+  const ta::KernelEntry& ke = bl->ke;
+  if (!ke.fn) return fail(TA_ERR_LOGIC, "no kernel instantiation for grid " + std::to_string(grid));
+  TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
+  int per_sm = 0;
+  TA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ke.fn, ke.threads, ke.smem));
+  if (per_sm < 1) return fail(TA_ERR_CUDA, "wavefront kernel does not fit on an SM");
+  const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
+  bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
+  StreamPlan plan;
+  plan_streams(ids, bt->a, bl->ctas, lanes, grid, &plan);
+  TA_CK(bl->items.reserve(plan.items.size()));
+  TA_CK(bl->soff.reserve(plan.soff.size()));
+  TA_CK(bl->steps.reserve(plan.steps.size()));
+  TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * 4, cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
+  bl->padded = 0;
+  for (int32_t id : ids) bl->padded += int64_t(bt->a[size_t(id)] + 1) * grid * grid * ta::kTileN * ta::kTileN;
+  return TA_OK;
+}
+
+int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st, int64_t* launches) {
+  ta::WaveArgs args = base;
+  args.items = bl->items.ptr;
+  args.stream_off = bl->soff.ptr;
+  args.cta_steps = bl->steps.ptr;
+  bl->ke.fn<<<bl->ctas, bl->ke.threads, bl->ke.smem, st>>>(args);
+  TA_CK(cudaGetLastError());
+  *launches += 1;
+  return TA_OK;
+}
+
+int launch_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
+                  bool trace, const ta::WaveArgs& base, cudaStream_t st, int64_t* launches) {
+  BucketLaunch bl;
+  if (int rc = prepare_bucket(bt, ids, grid, lanes, mode, trace, st, &bl)) return rc;
+  if (int rc = launch_prepared(&bl, base, st, launches)) return rc;
+  TA_CK(cudaStreamSynchronize(st));  // bl's buffers die here
+  bt->stats.padded_cells += bl.padded;
+  return TA_OK;
+}
+
+int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
+             ta_results* rows_out) {
+  const int64_t n = bt->n;
+  bt->stats = ta_stats{};
+  bt->status = bt->pre_status;
+  const bool rows = opt.with_rows != 0;
+  if (int rc = validate_scheme(scheme)) return rc;
+  if (opt.mode < 0 || opt.mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "unknown alignment mode");
+  // Per-triplet engine errors, exactly where the reference raises them:
+  // EngineConfig::validate + make_layout (tiled.cpp:8-15, 37-58) on the
+  // score path, the tensor budget (oracle.cpp:16-20) on the rows path.
+  const int cfg_rc = rows ? TA_OK : validate_options(opt);
+  const std::string cfg_msg = cfg_rc ? g_err : std::string();
+  std::vector<std::vector<int32_t>> buckets(ta::kNumGrid);
+  std::vector<int32_t> all_ok;
+  all_ok.reserve(size_t(n));
+  int max_a_bucket[ta::kNumGrid] = {0};
+  for (int64_t t = 0; t < n; ++t) {
+    if (bt->status[size_t(t)] != TA_OK) continue;
+    const int32_t A = bt->a[size_t(t)], B = bt->b[size_t(t)], C = bt->c[size_t(t)];
+    if (!rows) {
+      if (cfg_rc) {
+        bt->status[size_t(t)] = cfg_rc;
+        continue;
+      }
+      const uint64_t cells = uint64_t(A) * uint64_t(B) * uint64_t(C);
+      if (cells > opt.cell_budget) {
+        bt->status[size_t(t)] = TA_ERR_CAPACITY;
+        continue;
+      }
+      const int32_t width = opt.team_width > 0 ? opt.team_width : derive_team_width(opt.tile_size, B, C);
+      if (int64_t(width) * opt.tile_size < std::max(B, C)) {
+        bt->status[size_t(t)] = TA_ERR_CONFIG;
+        continue;
+      }
+    } else {
+      const uint64_t total = uint64_t(A + 1) * uint64_t(B + 1) * uint64_t(C + 1);
+      if (total > opt.cell_budget) {
+        bt->status[size_t(t)] = TA_ERR_CAPACITY;
+        continue;
+      }
+    }
+    if (opt.mode != TA_GLOBAL && uint64_t(A + 1) * uint64_t(B + 1) * uint64_t(C + 1) > 0xFFFFFFFFull) {
+      bt->status[size_t(t)] = TA_ERR_CAPACITY;  // lexicographic key needs < 2^32 cells
+      continue;
+    }
+    const int g = pick_grid(B, C);
+    if (g < 0) {
+      bt->status[size_t(t)] = TA_ERR_CAPACITY;  // long-triplet path not built yet
+      continue;
+    }
+    int gi = 0;
+    while (ta::kGridSizes[gi] != g) ++gi;
+    buckets[size_t(gi)].push_back(int32_t(t));
+    max_a_bucket[gi] = std::max(max_a_bucket[gi], A);
+    all_ok.push_back(int32_t(t));
+  }
+  if (cfg_rc) g_err = cfg_msg;
+
+  ta::WaveArgs base{};
+  base.seq = bt->seq.ptr;
+  base.desc = bt->d_desc.ptr;
+  base.out_score = bt->d_score.ptr;
+  base.out_end = bt->d_end.ptr;
+  base.out_key = bt->d_key.ptr;
+  base.g2 = 2 * scheme.gap;
+  base.match_p = scheme.match - base.g2;
+  base.mismatch_p = scheme.mismatch - base.g2;
+
+  if (!bt->ev0) TA_CK(cudaEventCreate(&bt->ev0));
+  if (!bt->ev1) TA_CK(cudaEventCreate(&bt->ev1));
+  if (opt.mode != TA_GLOBAL) TA_CK(cudaMemsetAsync(bt->d_key.ptr, 0, size_t(n) * 8, st));
+
+  int64_t launches = 0;
+  int lanes_used = 1;
+  int nbuckets = 0;
+  float ms_total = 0.f;
+  if (!rows) {
+    std::vector<std::unique_ptr<BucketLaunch>> prepared;
+    for (int gi = 0; gi < ta::kNumGrid; ++gi) {
+      if (buckets[size_t(gi)].empty()) continue;
+      const int g = ta::kGridSizes[gi];
+      const int lanes = s16_ok(scheme, max_a_bucket[gi], g) ? 2 : 1;
+      lanes_used = std::max(lanes_used, lanes);
+      ++nbuckets;
+      prepared.push_back(std::make_unique<BucketLaunch>());
+      if (int rc = prepare_bucket(bt, buckets[size_t(gi)], g, lanes, opt.mode, false, st, prepared.back().get()))
+        return rc;
+    }
+    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
+      TA_CK(bt->d_ids.reserve(all_ok.size()));
+      TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, all_ok.data(), all_ok.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    TA_CK(cudaEventRecord(bt->ev0, st));
+    for (auto& bl : prepared) {
+      if (int rc = launch_prepared(bl.get(), base, st, &launches)) return rc;
+      bt->stats.padded_cells += bl->padded;
+    }
+    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
+      const int64_t m = int64_t(all_ok.size());
+      decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr, m,
+                                                                  bt->d_score.ptr, bt->d_end.ptr);
+      TA_CK(cudaGetLastError());
+      ++launches;
+    }
+    TA_CK(cudaEventRecord(bt->ev1, st));
+    TA_CK(cudaEventSynchronize(bt->ev1));
+    TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
+  } else {
+    // Direction-cube chunks: (a+1) * G^2 tile-slices of 64 B per triplet.
+    size_t free_b = 0, total_b = 0;
+    TA_CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b) * 0.5));
+    TA_CK(cudaEventRecord(bt->ev0, st));
+    for (int gi = 0; gi < ta::kNumGrid; ++gi) {
+      const std::vector<int32_t>& ids = buckets[size_t(gi)];
+      if (ids.empty()) continue;
+      ++nbuckets;
+      const int g = ta::kGridSizes[gi];
+      size_t pos = 0;
+      while (pos < ids.size()) {
+        std::vector<int32_t> chunk;
+        std::vector<int64_t> diroff(size_t(n), 0);
+        size_t used = 0;  // uint4 units
+        while (pos < ids.size()) {
+          const int32_t id = ids[pos];
+          const size_t need = size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * 4;
+          if (!chunk.empty() && (used + need) * 16 > budget) break;
+          diroff[size_t(id)] = int64_t(used);
+          used += need;
+          chunk.push_back(id);
+          ++pos;
+        }
+        TA_CK(bt->d_dirs.reserve(used));
+        TA_CK(bt->d_diroff.reserve(size_t(n)));
+        TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        ta::WaveArgs args = base;
+        args.dirs = bt->d_dirs.ptr;
+        args.dir_off = bt->d_diroff.ptr;
+        if (int rc = launch_bucket(bt, chunk, g, 1, opt.mode, true, args, st, &launches)) return rc;
+        if (opt.mode != TA_GLOBAL) {
+          TA_CK(bt->d_ids.reserve(chunk.size()));
+          TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
+          const int64_t m = int64_t(chunk.size());
+          decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr,
+                                                                      m, bt->d_score.ptr, bt->d_end.ptr);
+          TA_CK(cudaGetLastError());
+          ++launches;
+        }
+        TA_CK(bt->d_ids.reserve(chunk.size()));
+        TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
+        const int m = int(chunk.size());
+        walker_kernel<<<unsigned((m + 127) / 128), 128, 0, st>>>(
+            bt->d_desc.ptr, bt->seq.ptr, bt->d_ids.ptr, m, reinterpret_cast<const uint32_t*>(bt->d_dirs.ptr),
+            bt->d_diroff.ptr, g, opt.mode, bt->d_end.ptr, bt->d_begin.ptr, bt->d_rows.ptr, bt->d_rowoff.ptr,
+            bt->d_rowlen.ptr, bt->d_status.ptr);
+        TA_CK(cudaGetLastError());
+        ++launches;
+        TA_CK(cudaStreamSynchronize(st));
+      }
+    }
+    TA_CK(cudaEventRecord(bt->ev1, st));
+    TA_CK(cudaEventSynchronize(bt->ev1));
+    TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
+  }
+  (void)rows_out;
+  int64_t cells = 0;
+  for (int32_t id : all_ok) cells += int64_t(bt->a[size_t(id)]) * bt->b[size_t(id)] * bt->c[size_t(id)];
+  bt->stats.kernel_ms = ms_total;
+  bt->stats.wavefront_ms = ms_total;
+  bt->stats.cells = cells;
+  bt->stats.launches = launches;
+  bt->stats.lanes = lanes_used;
+  bt->stats.buckets = nbuckets;
+  bt->last_mode = opt.mode;
+  bt->last_rows = rows;
+  return TA_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+
+extern "C" {
+
+const char* ta_last_error(void) { return g_err.c_str(); }
+
+const char* ta_version(void) { return "trioalign-b200 0.1 (sm_100a)"; }
+
+int ta_device_count(int* count) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) c = 0;
+  *count = c;
+  return TA_OK;
+}
+
+int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_t n,
+                    ta_batch** out, void* stream) {
+  *out = nullptr;
+  if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
+  DeviceCtx* ctx = nullptr;
+  if (int rc = get_ctx(device, &ctx)) return rc;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  auto bt = std::make_unique<ta_batch>();
+  bt->device = device;
+  bt->ctx = ctx;
+  bt->n = n;
+  bt->a.resize(size_t(n));
+  bt->b.resize(size_t(n));
+  bt->c.resize(size_t(n));
+  bt->desc.resize(size_t(n));
+  bt->pre_status.assign(size_t(n), TA_OK);
+  std::vector<int64_t> src_off(size_t(3 * n));
+  std::vector<int32_t> len(size_t(3 * n));
+  std::vector<uint32_t> dst_word(size_t(3 * n));
+  uint64_t words = 0;
+  for (int64_t t = 0; t < n; ++t) {
+    for (int d = 0; d < 3; ++d) {
+      const int64_t lo = offsets[3 * t + d], hi = offsets[3 * t + d + 1];
+      if (hi < lo || hi - lo > (int64_t(1) << 24))
+        return fail(TA_ERR_INVALID_ARGUMENT, "bad sequence offsets for triplet " + std::to_string(t));
+      src_off[size_t(3 * t + d)] = lo;
+      len[size_t(3 * t + d)] = int32_t(hi - lo);
+      dst_word[size_t(3 * t + d)] = uint32_t(words);
+      words += uint64_t((hi - lo + 15) / 16);
+    }
+    ta::TripletDesc& ds = bt->desc[size_t(t)];
+    ds.a = bt->a[size_t(t)] = len[size_t(3 * t)];
+    ds.b = bt->b[size_t(t)] = len[size_t(3 * t + 1)];
+    ds.c = bt->c[size_t(t)] = len[size_t(3 * t + 2)];
+    ds.flags = 0;
+    ds.w0 = dst_word[size_t(3 * t)];
+    ds.w1 = dst_word[size_t(3 * t + 1)];
+    ds.w2 = dst_word[size_t(3 * t + 2)];
+    ds.pad = 0;
+  }
+  if (words > 0xFFFFFFF0ull) return fail(TA_ERR_CAPACITY, "batch exceeds 2^32 packed words");
+  const int64_t first = n ? offsets[0] : 0;
+  const int64_t bytes = n ? offsets[3 * n] - first : 0;
+  for (auto& o : src_off) o -= first;
+  TA_CK(bt->seq.reserve(size_t(words) + 1));
+  TA_CK(bt->d_desc.reserve(size_t(n)));
+  TA_CK(bt->d_score.reserve(size_t(n)));
+  TA_CK(bt->d_end.reserve(size_t(3 * n)));
+  TA_CK(bt->d_status.reserve(size_t(n)));
+  TA_CK(bt->d_key.reserve(size_t(n)));
+  if (n > 0) {
+    DevBuf<char> ascii;
+    DevBuf<int64_t> d_src;
+    DevBuf<int32_t> d_len, d_bad;
+    DevBuf<uint32_t> d_dst;
+    TA_CK(ascii.reserve(size_t(bytes) + 1));
+    TA_CK(d_src.reserve(size_t(3 * n)));
+    TA_CK(d_len.reserve(size_t(3 * n)));
+    TA_CK(d_dst.reserve(size_t(3 * n)));
+    TA_CK(d_bad.reserve(size_t(n)));
+    TA_CK(cudaMemcpyAsync(ascii.ptr, seqs + first, size_t(bytes), cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(d_src.ptr, src_off.data(), size_t(3 * n) * 8, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(d_len.ptr, len.data(), size_t(3 * n) * 4, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(d_dst.ptr, dst_word.data(), size_t(3 * n) * 4, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bt->d_desc.ptr, bt->desc.data(), size_t(n) * sizeof(ta::TripletDesc),
+                          cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemsetAsync(d_bad.ptr, 0, size_t(n) * 4, st));
+    const int64_t nseq = 3 * n;
+    const int64_t threads = nseq * 32;
+    pack_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(ascii.ptr, d_src.ptr, d_len.ptr, d_dst.ptr,
+                                                               nseq, bt->seq.ptr, d_bad.ptr);
+    TA_CK(cudaGetLastError());
+    std::vector<int32_t> bad(static_cast<size_t>(n));
+    TA_CK(cudaMemcpyAsync(bad.data(), d_bad.ptr, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+    TA_CK(cudaStreamSynchronize(st));
+    for (int64_t t = 0; t < n; ++t)
+      if (bad[size_t(t)]) bt->pre_status[size_t(t)] = TA_ERR_PARSE;
+  }
+  *out = bt.release();
+  return TA_OK;
+}
+
+int ta_batch_run(ta_batch* b, const ta_scheme* scheme, const ta_options* opt, void* stream) {
+  if (!b || !scheme || !opt) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  TA_CK(cudaSetDevice(b->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->ctx->stream;
+  if (opt->with_rows) {
+    // rows need the row buffers; use ta_align_batch for the rows path
+    return fail(TA_ERR_INVALID_ARGUMENT, "ta_batch_run computes scores; rows go through ta_align_batch");
+  }
+  return run_impl(b, *scheme, *opt, st, nullptr);
+}
+
+int ta_batch_fetch(ta_batch* b, ta_results* out, void* stream) {
+  if (!b || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  TA_CK(cudaSetDevice(b->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->ctx->stream;
+  const size_t n = size_t(b->n);
+  if (n == 0) return TA_OK;
+  if (out->scores) TA_CK(cudaMemcpyAsync(out->scores, b->d_score.ptr, n * 4, cudaMemcpyDeviceToHost, st));
+  if (out->ends) TA_CK(cudaMemcpyAsync(out->ends, b->d_end.ptr, n * 12, cudaMemcpyDeviceToHost, st));
+  TA_CK(cudaStreamSynchronize(st));
+  if (out->status) std::memcpy(out->status, b->status.data(), n * 4);
+  for (size_t t = 0; t < n; ++t) {
+    if (b->status[t] != TA_OK) {
+      if (out->scores) out->scores[t] = 0;
+      if (out->ends) out->ends[3 * t] = out->ends[3 * t + 1] = out->ends[3 * t + 2] = 0;
+    }
+  }
+  return TA_OK;
+}
+
+int ta_batch_stats(const ta_batch* b, ta_stats* out) {
+  if (!b || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  *out = b->stats;
+  return TA_OK;
+}
+
+void ta_batch_destroy(ta_batch* b) {
+  if (!b) return;
+  cudaSetDevice(b->device);
+  delete b;
+}
+
+int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t n,
+                   const ta_scheme* scheme, const ta_options* opt, ta_results* out, void* stream) {
+  if (!scheme || !opt || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  ta_batch* bt = nullptr;
+  if (int rc = ta_batch_create(device, seqs, offsets, n, &bt, stream)) return rc;
+  std::unique_ptr<ta_batch, void (*)(ta_batch*)> guard(bt, ta_batch_destroy);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : bt->ctx->stream;
+  if (!opt->with_rows) {
+    if (int rc = run_impl(bt, *scheme, *opt, st, nullptr)) return rc;
+    return ta_batch_fetch(bt, out, stream);
+  }
+  // rows path: device row buffers sized a+b+c per row
+  const size_t nn = size_t(n);
+  std::vector<int64_t> roff(nn);
+  int64_t total = 0;
+  for (size_t t = 0; t < nn; ++t) {
+    roff[t] = total;
+    total += 3 * (int64_t(bt->a[t]) + bt->b[t] + bt->c[t]);
+  }
+  TA_CK(bt->d_rows.reserve(size_t(total) + 1));
+  TA_CK(bt->d_rowoff.reserve(nn));
+  TA_CK(bt->d_rowlen.reserve(nn));
+  TA_CK(bt->d_begin.reserve(3 * nn));
+  TA_CK(cudaMemsetAsync(bt->d_rowlen.ptr, 0, nn * 4, st));
+  TA_CK(cudaMemsetAsync(bt->d_begin.ptr, 0, nn * 12, st));
+  TA_CK(cudaMemsetAsync(bt->d_status.ptr, 0, nn * 4, st));
+  if (nn) TA_CK(cudaMemcpyAsync(bt->d_rowoff.ptr, roff.data(), nn * 8, cudaMemcpyHostToDevice, st));
+  if (int rc = run_impl(bt, *scheme, *opt, st, out)) return rc;
+  if (nn == 0) return TA_OK;
+  std::vector<int32_t> dstat(nn), rlen(nn), beg(3 * nn);
+  std::vector<char> rows(size_t(total) + 1);
+  TA_CK(cudaMemcpyAsync(dstat.data(), bt->d_status.ptr, nn * 4, cudaMemcpyDeviceToHost, st));
+  TA_CK(cudaMemcpyAsync(rlen.data(), bt->d_rowlen.ptr, nn * 4, cudaMemcpyDeviceToHost, st));
+  TA_CK(cudaMemcpyAsync(beg.data(), bt->d_begin.ptr, nn * 12, cudaMemcpyDeviceToHost, st));
+  TA_CK(cudaMemcpyAsync(rows.data(), bt->d_rows.ptr, size_t(total), cudaMemcpyDeviceToHost, st));
+  TA_CK(cudaStreamSynchronize(st));
+  for (size_t t = 0; t < nn; ++t)
+    if (bt->status[t] == TA_OK && dstat[t] != TA_OK) bt->status[t] = dstat[t];
+  if (int rc = ta_batch_fetch(bt, out, stream)) return rc;
+  for (size_t t = 0; t < nn; ++t) {
+    const bool ok = bt->status[t] == TA_OK;
+    if (out->begins) {
+      for (int d = 0; d < 3; ++d) out->begins[3 * t + d] = ok ? beg[3 * t + d] : 0;
+    }
+    if (out->row_lens) out->row_lens[t] = ok ? rlen[t] : 0;
+    if (ok && out->rows0 && out->row_offsets) {
+      const int64_t cap = int64_t(bt->a[t]) + bt->b[t] + bt->c[t];
+      const char* src = rows.data() + roff[t];
+      std::memcpy(out->rows0 + out->row_offsets[t], src, size_t(rlen[t]));
+      std::memcpy(out->rows1 + out->row_offsets[t], src + cap, size_t(rlen[t]));
+      std::memcpy(out->rows2 + out->row_offsets[t], src + 2 * cap, size_t(rlen[t]));
+    }
+  }
+  return TA_OK;
+}
+
+int64_t ta_packed_score_bound(int64_t a, int64_t b, int64_t c, const ta_scheme* s) {
+  const int64_t per = std::max({3 * std::abs(int64_t(s->match)), 3 * std::abs(int64_t(s->mismatch)),
+                                2 * std::abs(int64_t(s->gap))});
+  return (a + b + c) * per;
+}
+
+int32_t ta_derive_team_width(int32_t tile_size, int32_t b, int32_t c) {
+  return derive_team_width(tile_size, b, c);
+}
+
+int ta_validate_scheme(const ta_scheme* s) { return validate_scheme(*s); }
+
+int ta_validate_options(const ta_options* o) { return validate_options(*o); }
+
+int ta_plan_partition(const uint64_t* cells, int64_t n, int32_t strategy, int32_t workers,
+                      int32_t* assignment) {
+  // dispatch.cpp:29-60
+  if (workers < 1) return fail(TA_ERR_CONFIG, "worker count must be >= 1");
+  if (n <= 0) return fail(TA_ERR_CONFIG, "cannot partition an empty dataset");
+  switch (strategy) {
+    case 0: {
+      const int64_t chunk = (n + workers - 1) / workers;
+      for (int64_t i = 0; i < n; ++i) assignment[i] = int32_t(i / chunk);
+      break;
+    }
+    case 1:
+      for (int64_t i = 0; i < n; ++i) assignment[i] = int32_t(i % workers);
+      break;
+    case 2: {
+      std::vector<uint64_t> load(size_t(workers), 0);
+      for (int64_t i = 0; i < n; ++i) {
+        int32_t best = 0;
+        for (int32_t w = 1; w < workers; ++w)
+          if (load[size_t(w)] < load[size_t(best)]) best = w;
+        assignment[i] = best;
+        load[size_t(best)] += cells[i];
+      }
+      break;
+    }
+    default:
+      return fail(TA_ERR_PARSE, "unknown partition strategy");
+  }
+  return TA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// kernels.h — instantiation table of the wavefront kernel family.
+// Each tile-grid size G lives in its own translation unit (kernels_gXX.cu)
+// so the heavy unrolled instantiations compile in parallel.
+#pragma once
+
+#include <cstddef>
+
+#include "wavefront.cuh"
+
+namespace ta {
+
+constexpr int kTileN = 10;                 // cells per tile side
+constexpr int kGridSizes[] = {4, 8, 12, 16};  // tile-grid sides (plane extent G*N)
+constexpr int kNumGrid = sizeof(kGridSizes) / sizeof(kGridSizes[0]);
+constexpr int kMaxExtent = 16 * kTileN;    // largest single-block plane side
+
+using WaveFn = void (*)(WaveArgs);
+
+struct KernelEntry {
+  WaveFn fn = nullptr;
+  size_t smem = 0;
+  int threads = 0;
+  int grid = 0;
+};
+
+// lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace requires lanes == 1.
+KernelEntry kernel_g4(int lanes, int mode, bool trace);
+KernelEntry kernel_g8(int lanes, int mode, bool trace);
+KernelEntry kernel_g12(int lanes, int mode, bool trace);
+KernelEntry kernel_g16(int lanes, int mode, bool trace);
+
+inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace) {
+  switch (grid) {
+    case 4: return kernel_g4(lanes, mode, trace);
+    case 8: return kernel_g8(lanes, mode, trace);
+    case 12: return kernel_g12(lanes, mode, trace);
+    case 16: return kernel_g16(lanes, mode, trace);
+  }
+  return {};
+}
+
+}  // namespace ta
+
+#define TA_DEFINE_KERNEL_TABLE(G)                                                      \
+  namespace ta {                                                                       \
+  template <int L, int M, bool TR>                                                     \
+  static KernelEntry entry_##G() {                                                     \
+    return KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR>,                         \
+                       WaveSmem<kTileN, G, L>::bytes, G * G, G};                       \
+  }                                                                                    \
+  KernelEntry kernel_g##G(int lanes, int mode, bool trace) {                           \
+    if (trace) {                                                                       \
+      if (lanes != 1) return {};                                                       \
+      switch (mode) {                                                                  \
+        case kGlobal: return entry_##G<1, kGlobal, true>();                            \
+        case kSemi: return entry_##G<1, kSemi, true>();                                \
+        case kLocal: return entry_##G<1, kLocal, true>();                              \
+      }                                                                                \
+      return {};                                                                       \
+    }                                                                                  \
+    if (lanes == 1) {                                                                  \
+      switch (mode) {                                                                  \
+        case kGlobal: return entry_##G<1, kGlobal, false>();                           \
+        case kSemi: return entry_##G<1, kSemi, false>();                               \
+        case kLocal: return entry_##G<1, kLocal, false>();                             \
+      }                                                                                \
+    } else {                                                                           \
+      switch (mode) {                                                                  \
+        case kGlobal: return entry_##G<2, kGlobal, false>();                           \
+        case kSemi: return entry_##G<2, kSemi, false>();                               \
+        case kLocal: return entry_##G<2, kLocal, false>();                             \
+      }                                                                                \
+    }                                                                                  \
+    return {};                                                                         \
+  }                                                                                    \
+  }

@@ -1,0 +1,167 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the oracle and
+the reference's own golden vectors.  Bit-exact (integer DP).  Needs a B200."""
+import numpy as np
+import pytest
+
+import paper_2605_28400_b200 as ta
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+MODES = (0, 1, 2)
+
+
+def trips_to_arrays(trips):
+    parts, offs, pos = [], [0], 0
+    for t in trips:
+        for s in t:
+            parts.append(s.encode())
+            pos += len(s)
+            offs.append(pos)
+    return np.frombuffer(b"".join(parts) + b"\0", np.uint8), np.asarray(offs, np.int64)
+
+
+def run(trips, scheme, mode, rows=False):
+    seqs, offs = trips_to_arrays(trips)
+    return ta.align_arrays(seqs, offs, ta.ScoringScheme(*scheme), ta.AlignmentMode(mode),
+                           with_rows=rows, cell_budget=(1 << 40) if rows else None)
+
+
+def test_kat(gpu_engine):
+    for case in load_golden("kat.json"):
+        out = run([case["t"]], case["scheme"], case["mode"], rows=True)
+        want = case["oracle"]
+        assert int(out["status"][0]) == 0
+        assert int(out["score"][0]) == want["score"], case
+        assert list(out["end"][0]) == want["end"], case
+        assert list(out["begin"][0]) == want["begin"], case
+        assert list(out["rows"][0]) == want["rows"], case
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_small_corpus_scores_and_rows(gpu_engine, mode):
+    cases = [c for c in load_golden("small_rows.json.gz") if c["mode"] == mode]
+    by_scheme = {}
+    for c in cases:
+        by_scheme.setdefault(tuple(c["scheme"]), []).append(c)
+    for sch, cs in by_scheme.items():
+        trips = [c["t"] for c in cs]
+        score_only = run(trips, sch, mode)
+        with_rows = run(trips, sch, mode, rows=True)
+        for x, c in enumerate(cs):
+            want = c["oracle"]
+            assert int(score_only["status"][x]) == 0
+            assert int(score_only["score"][x]) == want["score"], (sch, c["t"])
+            assert list(score_only["end"][x]) == want["end"], (sch, c["t"])
+            assert int(with_rows["score"][x]) == want["score"]
+            assert list(with_rows["end"][x]) == want["end"]
+            assert list(with_rows["begin"][x]) == want["begin"], (sch, c["t"])
+            assert list(with_rows["rows"][x]) == want["rows"], (sch, c["t"])
+
+
+def test_c1_all_rows_global(gpu_engine):
+    c1 = load_golden("c1_rows.json.gz")
+    from oracle.pyoracle import Oracle
+    seqs, offs = Oracle().generate(c1["spec"], c1["rates"][0], c1["rates"][1], c1["seed"])
+    for mode, recs in c1["modes"].items():
+        n = len(recs)
+        out = ta.align_arrays(seqs, offs[:3 * n + 1], ta.ScoringScheme(*c1["scheme"]),
+                              ta.AlignmentMode(int(mode)), with_rows=True, cell_budget=1 << 40)
+        sc = ta.align_arrays(seqs, offs[:3 * n + 1], ta.ScoringScheme(*c1["scheme"]),
+                             ta.AlignmentMode(int(mode)))
+        for t in range(n):
+            w = recs[t]
+            assert int(out["score"][t]) == w["score"] and int(sc["score"][t]) == w["score"], t
+            assert list(out["end"][t]) == w["end"] and list(sc["end"][t]) == w["end"], t
+            assert list(out["begin"][t]) == w["begin"], t
+            assert list(out["rows"][t]) == w["rows"], t
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_random_vs_oracle_many_lengths(gpu_engine, oracle, mode):
+    rng = np.random.default_rng(1234 + mode)
+    for sch in [(1, -1, -2), (2, -1, -2), (3, -2, -1), (1, 0, 0), (5, -4, -1), (7, -30, -20)]:
+        trips = []
+        for _ in range(60):
+            lens = rng.integers(0, 60, size=3)
+            if rng.random() < 0.2:
+                lens = rng.integers(90, 159, size=3)
+            trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in lens))
+        out = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.align(t, sch, mode)
+            assert int(out["status"][x]) == 0
+            assert int(out["score"][x]) == want["score"], (sch, mode, t)
+            assert list(out["end"][x]) == want["end"], (sch, mode, t)
+
+
+def test_config_samples_vs_reference(gpu_engine, oracle):
+    cfgs = load_golden("configs.json.gz")
+    for name in ("C2", "C3"):
+        ent = cfgs[name]
+        seqs, offs = oracle.generate(ent["sample_spec"], ent["rates"][0], ent["rates"][1], ent["seed"])
+        for mode, recs in ent["modes"].items():
+            n = len(recs)
+            out = ta.align_arrays(seqs, offs[:3 * n + 1], ta.ScoringScheme(*ent["scheme"]),
+                                  ta.AlignmentMode(int(mode)))
+            for t in range(n):
+                if max(ent["lengths"][t][1:]) >= 160:
+                    continue
+                assert int(out["score"][t]) == recs[t]["score"], (name, mode, t)
+                assert list(out["end"][t]) == recs[t]["end"], (name, mode, t)
+        if "rows_global" in ent:
+            k = len(ent["rows_global"])
+            out = ta.align_arrays(seqs, offs[:3 * k + 1], ta.ScoringScheme(*ent["scheme"]),
+                                  ta.AlignmentMode.Global, with_rows=True, cell_budget=1 << 40)
+            for t in range(k):
+                if max(ent["lengths"][t][1:]) >= 160:
+                    continue
+                assert list(out["rows"][t]) == ent["rows_global"][t]["rows"], (name, t)
+
+
+def test_reference_api_errors(gpu_engine):
+    t = ta.Triplet("t", "ACGTACGT", "ACGTACGT", "ACGTACGT")
+    cfg = ta.EngineConfig(tile_size=4, cell_budget=10)
+    with pytest.raises(ta.CapacityError):
+        ta.align(t, ta.ScoringScheme(), ta.AlignmentMode.Global, cfg)
+    with pytest.raises(ta.ConfigError):
+        ta.align(t, ta.ScoringScheme(), ta.AlignmentMode.Global, ta.EngineConfig(tile_size=2, team_width=2))
+    a = ta.Triplet("a", "ACGT", "AC", "G")
+    b = ta.Triplet("b", "ACG", "AC", "G")
+    with pytest.raises(ta.ShapeMismatchError):
+        ta.align_packed(a, b, ta.ScoringScheme(), ta.AlignmentMode.Global, ta.EngineConfig(tile_size=4))
+    big = ta.Triplet("big", "A" * 32, "A" * 32, "A" * 32)
+    with pytest.raises(ta.LaneOverflowError):
+        ta.align_packed(big, big, ta.ScoringScheme(5, -1, -300), ta.AlignmentMode.Global, ta.EngineConfig())
+    with pytest.raises(ta.CapacityError):
+        ta.oracle_align(ta.Triplet("big", "ACGTACGT", "ACGTACGT", "ACGTACGT"), ta.ScoringScheme(),
+                        ta.AlignmentMode.Global, True, 100)
+    r = ta.align(ta.Triplet("id", "ACG", "ACG", "ACG"), ta.ScoringScheme(2, -1, -2),
+                 ta.AlignmentMode.Global, ta.EngineConfig(tile_size=2))
+    assert r.score == 18 and r.end == (3, 3, 3)
+
+
+def test_run_batch_failures_recorded(gpu_engine):
+    data = [ta.Triplet(f"t{i}", "ACGT", "ACGA", "AGGT") for i in range(3)]
+    data.insert(1, ta.Triplet("too-big", "A" * 40, "A" * 40, "A" * 40))
+    cells = [t.cell_count() for t in data]
+    cfg = ta.EngineConfig(tile_size=4, cell_budget=10000)
+    rep = ta.run_batch(data, ta.ScoringScheme(), ta.AlignmentMode.Global, cfg,
+                       ta.plan_partition(cells, ta.Strategy.Interleaved, 2))
+    assert [o.ok for o in rep.per_triplet] == [True, False, True, True]
+    assert "budget" in rep.per_triplet[1].error
+    assert rep.scored_cells == sum(o.cells for o in rep.per_triplet if o.ok)
+
+
+def test_empty_and_degenerate(gpu_engine):
+    trips = [("", "", ""), ("A", "", ""), ("", "C", ""), ("", "", "G"), ("ACGT", "", ""),
+             ("", "ACGT", "TTTT"), ("A", "A", ""), ("T" * 150, "", "A" * 150)]
+    from oracle.pyoracle import Oracle
+    o = Oracle()
+    for mode in MODES:
+        out = run(trips, (1, -1, -2), mode, rows=True)
+        for x, t in enumerate(trips):
+            want = o.align(t, (1, -1, -2), mode, with_rows=True)
+            assert int(out["score"][x]) == want["score"], (mode, t)
+            assert list(out["end"][x]) == want["end"], (mode, t)
+            assert list(out["rows"][x]) == want["rows"], (mode, t)
