@@ -2,9 +2,9 @@
  * trioalign_capi.h — the C-ABI drop-in boundary of the B200 `trioalign` engine.
  *
  * The reference (/root/reference/proj) has no FFI layer: its "operator API" is
- * the C++ library (proj/include/trioalign/*.hpp) and the CLI.  This header is
+ * the C++ library (proj/include/trioalign/ headers) and the CLI.  This header is
  * the plain-pointer boundary underneath our reference-compatible C++ API
- * (paper_2605_28400_b200/csrc/include/trioalign/*.hpp) and the Python/ctypes
+ * (paper_2605_28400_b200/csrc/include/trioalign/ headers) and the Python/ctypes
  * binding.  Each entry point names the reference interface it replaces.
  *
  * Conventions: all pointers are host pointers unless stated; sizes are int64;
@@ -129,6 +129,23 @@ int ta_validate_options(const ta_options* opt);
  * 2 dynamic; assignment receives n worker indices. */
 int ta_plan_partition(const uint64_t* cell_counts, int64_t n, int32_t strategy,
                       int32_t workers, int32_t* assignment);
+
+/* ---- seeded synthetic datasets (support for `generate` / `bench --spec`) --
+ * generate_dataset (dataset.cpp:121-211) + DatasetSpec::parse (dataset.cpp:87-119),
+ * bit-identical, parallel over triplets.  *seqs / *offsets (3n+1) are malloc'd:
+ * release with ta_free.  Errors: TA_ERR_PARSE (message via ta_generate_error). */
+int ta_generate(const char* spec, double mutation, double indel, uint64_t seed, int threads,
+                char** seqs, int64_t** offsets, int64_t* n);
+/* Triplets [begin, end) of the same dataset (per-rank shards); end < 0 = all. */
+int ta_generate_slice(const char* spec, double mutation, double indel, uint64_t seed,
+                      int64_t begin, int64_t end, int threads, char** seqs, int64_t** offsets,
+                      int64_t* n);
+/* The recorded true alignment rows (generate --ref-out): triplet t's rows are
+ * ref[ref_off[t] + d*ref_len[t] ...] for d = 0..2; ref_len[t] < 0 = none. */
+int ta_generate_reference(const char* spec, double mutation, double indel, uint64_t seed,
+                          char** ref, int64_t** ref_off, int64_t** ref_len, int64_t* n);
+const char* ta_generate_error(void);
+void ta_free(void* p);
 
 #ifdef __cplusplus
 }

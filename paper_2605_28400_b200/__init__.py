@@ -24,6 +24,7 @@ __all__ = [
     "strategy_from_name", "PartitionPlan", "TripletOutcome", "WorkerStats", "BatchReport",
     "align", "align_packed", "oracle_align", "run_batch", "plan_partition", "packed_score_bound",
     "packed_bound_ok", "derive_team_width", "tcups", "align_arrays", "DeviceBatch", "lib",
+    "generate", "triplets_from_arrays", "device_count",
     "TrioalignError", "ParseError", "CapacityError", "ConfigError", "ShapeMismatchError",
     "LaneOverflowError", "MalformedAlignmentError", "LogicError", "CudaError", "KGAP",
     "K_ORACLE_CELL_BUDGET", "LIB_PATH",
@@ -123,7 +124,8 @@ EXPORTED_SYMBOLS = (
     "ta_last_error", "ta_version", "ta_device_count", "ta_align_batch", "ta_batch_create",
     "ta_batch_run", "ta_batch_fetch", "ta_batch_stats", "ta_batch_destroy",
     "ta_packed_score_bound", "ta_derive_team_width", "ta_validate_scheme",
-    "ta_validate_options", "ta_plan_partition",
+    "ta_validate_options", "ta_plan_partition", "ta_generate", "ta_generate_slice", "ta_generate_reference",
+    "ta_generate_error", "ta_free",
 )
 
 
@@ -155,6 +157,16 @@ def lib() -> ctypes.CDLL:
     L.ta_validate_scheme.argtypes = [ctypes.POINTER(_Scheme)]
     L.ta_validate_options.argtypes = [ctypes.POINTER(_Options)]
     L.ta_plan_partition.argtypes = [vp, i64, i32, i32, vp]
+    L.ta_generate.argtypes = [ctypes.c_char_p, ctypes.c_double, ctypes.c_double, u64, ctypes.c_int,
+                              ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.ta_generate_slice.argtypes = [ctypes.c_char_p, ctypes.c_double, ctypes.c_double, u64, i64, i64,
+                                    ctypes.c_int, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(i64)]
+    L.ta_generate_reference.argtypes = [ctypes.c_char_p, ctypes.c_double, ctypes.c_double, u64,
+                                        ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                        ctypes.POINTER(i64)]
+    L.ta_generate_error.restype = ctypes.c_char_p
+    L.ta_free.argtypes = [vp]
+    L.ta_free.restype = None
     _LIB = L
     return L
 
@@ -312,6 +324,39 @@ def tcups(cells: int, seconds: float) -> float:  # metrics.cpp:11-14
     if seconds <= 0:
         raise ValueError("tcups: runtime must be positive")
     return cells / (seconds * 1e12)
+
+
+# ---------------------------------------------------------------------------
+# seeded synthetic datasets (dataset.cpp:87-211, bit-identical, parallel)
+
+def generate(spec: str, mutation: float = 0.0, indel: float = 0.0, seed: int = 0,
+             threads: int = 0, begin: int = 0, end: int = -1) -> Tuple[np.ndarray, np.ndarray]:
+    """`trioalign generate --spec SPEC --rates M:I --seed S` as arrays:
+    (seqs uint8 ASCII, offsets int64 [3n+1]); [begin, end) selects a shard."""
+    L = lib()
+    s, o, n = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int64()
+    rc = L.ta_generate_slice(spec.encode(), float(mutation), float(indel), int(seed), int(begin),
+                             int(end), int(threads), ctypes.byref(s), ctypes.byref(o), ctypes.byref(n))
+    if rc:
+        _raise(rc, L.ta_generate_error().decode())
+    try:
+        offs = np.ctypeslib.as_array(ctypes.cast(o, ctypes.POINTER(ctypes.c_int64)),
+                                     shape=(3 * n.value + 1,)).copy()
+        total = int(offs[-1])
+        seqs = np.empty(total + 1, np.uint8)
+        ctypes.memmove(seqs.ctypes.data, s, total)
+        seqs[total] = 0
+    finally:
+        L.ta_free(s)
+        L.ta_free(o)
+    return seqs, offs
+
+
+def triplets_from_arrays(seqs: np.ndarray, offsets: np.ndarray, prefix: str = "t") -> List[Triplet]:
+    raw = seqs.tobytes()
+    n = (len(offsets) - 1) // 3
+    return [Triplet(f"{prefix}{t}", *(raw[offsets[3 * t + d]:offsets[3 * t + d + 1]].decode()
+                                        for d in range(3))) for t in range(n)]
 
 
 # ---------------------------------------------------------------------------

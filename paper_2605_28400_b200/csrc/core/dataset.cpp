@@ -226,23 +226,28 @@ const char* ta_generate_error(void) { return g_gen_err.c_str(); }
 
 void ta_free(void* p) { std::free(p); }
 
-int ta_generate(const char* spec, double mutation, double indel, uint64_t seed, int threads,
-                char** seqs_out, int64_t** offsets_out, int64_t* n_out) {
+int ta_generate_slice(const char* spec, double mutation, double indel, uint64_t seed,
+                      int64_t begin, int64_t end, int threads, char** seqs_out,
+                      int64_t** offsets_out, int64_t* n_out) {
   *seqs_out = nullptr;
   *offsets_out = nullptr;
   *n_out = 0;
   Spec sp;
   if (int rc = parse_spec(spec ? spec : "", mutation, indel, &sp)) return rc;
-  const int64_t n = sp.count;
+  if (end < 0 || end > sp.count) end = sp.count;
+  if (begin < 0) begin = 0;
+  if (begin > end) begin = end;
+  const int64_t n = end - begin;
   if (threads < 1) threads = int(std::max(1u, std::thread::hardware_concurrency()));
   threads = int(std::min<int64_t>(threads, std::max<int64_t>(1, n / 64)));
-  std::vector<std::string> chunk(size_t(threads));
-  std::vector<int64_t> lens(size_t(3 * n));
+  std::vector<std::string> chunk(static_cast<size_t>(threads));
+  std::vector<int64_t> lens(static_cast<size_t>(3 * n));
   std::vector<std::thread> pool;
   for (int w = 0; w < threads; ++w) {
     pool.emplace_back([&, w] {
       const int64_t lo = n * w / threads, hi = n * (w + 1) / threads;
-      for (int64_t t = lo; t < hi; ++t) gen_one(sp, mutation, indel, seed, t, &chunk[size_t(w)], &lens[size_t(3 * t)], nullptr, nullptr);
+      for (int64_t t = lo; t < hi; ++t)
+        gen_one(sp, mutation, indel, seed, begin + t, &chunk[size_t(w)], &lens[size_t(3 * t)], nullptr, nullptr);
     });
   }
   for (auto& th : pool) th.join();
@@ -273,6 +278,11 @@ int ta_generate(const char* spec, double mutation, double indel, uint64_t seed, 
   return TA_OK;
 }
 
+int ta_generate(const char* spec, double mutation, double indel, uint64_t seed, int threads,
+                char** seqs_out, int64_t** offsets_out, int64_t* n_out) {
+  return ta_generate_slice(spec, mutation, indel, seed, 0, -1, threads, seqs_out, offsets_out, n_out);
+}
+
 // Reference rows of a generated dataset (the `generate --ref-out` payload):
 // rows of triplet t are ref[ref_off[t] .. ) as three consecutive rows of
 // length ref_len[t]; ref_len < 0 when the spec records no alignment.
@@ -286,7 +296,7 @@ int ta_generate_reference(const char* spec, double mutation, double indel, uint6
   if (int rc = parse_spec(spec ? spec : "", mutation, indel, &sp)) return rc;
   const int64_t n = sp.count;
   std::string all, scratch;
-  std::vector<int64_t> off(size_t(n)), rl(size_t(n));
+  std::vector<int64_t> off(static_cast<size_t>(n)), rl(static_cast<size_t>(n));
   int64_t lens[3];
   for (int64_t t = 0; t < n; ++t) {
     off[size_t(t)] = int64_t(all.size());

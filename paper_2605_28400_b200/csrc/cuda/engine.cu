@@ -62,6 +62,15 @@ struct DevBuf {
   }
 };
 
+struct BucketLaunch {
+  int grid = 0, lanes = 0, mode = 0;
+  ta::KernelEntry ke;
+  int ctas = 0;
+  DevBuf<int32_t> items, soff, steps;
+  int64_t padded = 0;
+};
+
+
 // ---------------------------------------------------------------------------
 // kernels around the wavefront
 
@@ -335,6 +344,10 @@ struct ta_batch {
   DevBuf<char> d_rows;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   ta_stats stats{};
+  // score-path launch plans of the last run (reused while the bucket
+  // contents, lanes and mode are unchanged)
+  std::vector<std::unique_ptr<BucketLaunch>> plan_cache;
+  std::string plan_key;
   int last_mode = -1;
   bool last_rows = false;
   ~ta_batch() {
@@ -358,7 +371,7 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
   using Load = std::pair<int64_t, int32_t>;
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
   for (int s = 0; s < S; ++s) heap.push({0, s});
-  std::vector<int64_t> load(size_t(S), 0);
+  std::vector<int64_t> load(static_cast<size_t>(S), 0);
   for (int32_t id : ids) {
     Load top = heap.top();
     heap.pop();
@@ -382,16 +395,12 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
   }
 }
 
-struct BucketLaunch {
-  ta::KernelEntry ke;
-  int ctas = 0;
-  DevBuf<int32_t> items, soff, steps;
-  int64_t padded = 0;
-};
-
 // Host planning + upload for one bucket (outside any timed region).
 int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
                    bool trace, cudaStream_t st, BucketLaunch* bl) {
+  bl->grid = grid;
+  bl->lanes = lanes;
+  bl->mode = mode;
   bl->ke = ta::lookup_kernel(grid, lanes, mode, trace);
   const ta::KernelEntry& ke = bl->ke;
   if (!ke.fn) return fail(TA_ERR_LOGIC, "no kernel instantiation for grid " + std::to_string(grid));
@@ -513,23 +522,39 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   int nbuckets = 0;
   float ms_total = 0.f;
   if (!rows) {
-    std::vector<std::unique_ptr<BucketLaunch>> prepared;
+    // plan key: mode + per-bucket (grid, lanes, ids) fingerprint
+    std::string key = std::to_string(opt.mode);
+    std::vector<int> lanes_of(ta::kNumGrid, 1);
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       if (buckets[size_t(gi)].empty()) continue;
-      const int g = ta::kGridSizes[gi];
-      const int lanes = s16_ok(scheme, max_a_bucket[gi], g) ? 2 : 1;
-      lanes_used = std::max(lanes_used, lanes);
+      lanes_of[size_t(gi)] = s16_ok(scheme, max_a_bucket[gi], ta::kGridSizes[gi]) ? 2 : 1;
+      uint64_t h = 1469598103934665603ull;
+      for (int32_t id : buckets[size_t(gi)]) h = (h ^ uint64_t(id)) * 1099511628211ull;
+      key += "|" + std::to_string(ta::kGridSizes[gi]) + ":" + std::to_string(lanes_of[size_t(gi)]) + ":" +
+             std::to_string(buckets[size_t(gi)].size()) + ":" + std::to_string(h);
+    }
+    if (key != bt->plan_key) {
+      bt->plan_cache.clear();
+      bt->plan_key.clear();
+      for (int gi = 0; gi < ta::kNumGrid; ++gi) {
+        if (buckets[size_t(gi)].empty()) continue;
+        bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
+        if (int rc = prepare_bucket(bt, buckets[size_t(gi)], ta::kGridSizes[gi], lanes_of[size_t(gi)], opt.mode,
+                                    false, st, bt->plan_cache.back().get()))
+          return rc;
+      }
+      bt->plan_key = key;
+    }
+    for (auto& bl : bt->plan_cache) {
+      lanes_used = std::max(lanes_used, bl->lanes);
       ++nbuckets;
-      prepared.push_back(std::make_unique<BucketLaunch>());
-      if (int rc = prepare_bucket(bt, buckets[size_t(gi)], g, lanes, opt.mode, false, st, prepared.back().get()))
-        return rc;
     }
     if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
       TA_CK(bt->d_ids.reserve(all_ok.size()));
       TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, all_ok.data(), all_ok.size() * 4, cudaMemcpyHostToDevice, st));
     }
     TA_CK(cudaEventRecord(bt->ev0, st));
-    for (auto& bl : prepared) {
+    for (auto& bl : bt->plan_cache) {
       if (int rc = launch_prepared(bl.get(), base, st, &launches)) return rc;
       bt->stats.padded_cells += bl->padded;
     }
@@ -557,7 +582,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       size_t pos = 0;
       while (pos < ids.size()) {
         std::vector<int32_t> chunk;
-        std::vector<int64_t> diroff(size_t(n), 0);
+        std::vector<int64_t> diroff(static_cast<size_t>(n), 0);
         size_t used = 0;  // uint4 units
         while (pos < ids.size()) {
           const int32_t id = ids[pos];
@@ -649,9 +674,9 @@ int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_
   bt->c.resize(size_t(n));
   bt->desc.resize(size_t(n));
   bt->pre_status.assign(size_t(n), TA_OK);
-  std::vector<int64_t> src_off(size_t(3 * n));
-  std::vector<int32_t> len(size_t(3 * n));
-  std::vector<uint32_t> dst_word(size_t(3 * n));
+  std::vector<int64_t> src_off(static_cast<size_t>(3 * n));
+  std::vector<int32_t> len(static_cast<size_t>(3 * n));
+  std::vector<uint32_t> dst_word(static_cast<size_t>(3 * n));
   uint64_t words = 0;
   for (int64_t t = 0; t < n; ++t) {
     for (int d = 0; d < 3; ++d) {
@@ -842,7 +867,7 @@ int ta_plan_partition(const uint64_t* cells, int64_t n, int32_t strategy, int32_
       for (int64_t i = 0; i < n; ++i) assignment[i] = int32_t(i % workers);
       break;
     case 2: {
-      std::vector<uint64_t> load(size_t(workers), 0);
+      std::vector<uint64_t> load(static_cast<size_t>(workers), 0);
       for (int64_t i = 0; i < n; ++i) {
         int32_t best = 0;
         for (int32_t w = 1; w < workers; ++w)

@@ -128,14 +128,21 @@ struct WaveSmem {
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
   static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
-  static constexpr size_t bytes = kSig + 2 * kTab + kX;
+  static constexpr int kLaneFields = 8;                    // cold per-lane state
+  static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
+  static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane;
 };
+
+
+// Cold per-lane fields kept in shared memory ([lane][field][thread]).
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kBestV, kBestLin };
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE>
 __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args) {
   static_assert(!TRACE || LANES == 1, "direction cube uses int32 lanes");
   static_assert((N * N) % 4 == 0, "tile cells must group by 4");
+  static_assert(N <= 15, "a tile row's codes must fit one 32-bit word");
   static_assert(!TRACE || (N * N) <= 128, "direction slot is 64 B per tile-slice");
   using Ops = LaneOps<LANES>;
   using SM = WaveSmem<N, G, LANES>;
@@ -144,85 +151,137 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   constexpr int XW = SM::XW;
   constexpr int SH = TRACE ? 4 : 0;  // value scale 2^SH (tags in low bits)
   constexpr uint32_t NEG = TRACE ? 0xF0000000u : Ops::kNeg;
+  constexpr uint32_t kDone = 1u, kOwner = 2u, kBestOk = 4u;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint4* const s12v = reinterpret_cast<uint4*>(smem_raw);                         // [NN/4][T]
+  uint4* const s12v = reinterpret_cast<uint4*>(smem_raw);                     // [NN/4][T]
   uint32_t* const s12w = reinterpret_cast<uint32_t*>(smem_raw);
-  unsigned char* const tab1 = smem_raw + SM::kSig;                                // 8 B per (p, t)
+  unsigned char* const tab1 = smem_raw + SM::kSig;                            // 8 B per (row, thread)
   unsigned char* const tab2 = tab1 + SM::kTab;
-  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);            // [2][XW][T+1]
+  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);        // [2][XW][T+1]
+  int32_t* const lst = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX);  // [LANES][8][T]
 
   const int t = threadIdx.x;
-  const int r = t / G;
-  const int cc = t - r * G;
+  // Thread -> tile map in anti-diagonal order: a warp spans only 2-3
+  // pipeline skews (r + c), so per-triplet work at lane switches is not
+  // replayed by many divergent subsets of the warp.
+  int r, cc;
+  {
+    int rem = t, d = 0;
+    for (; d < 2 * G - 1; ++d) {
+      const int cnt = min(d, 2 * G - 2 - d) + 1;
+      if (rem < cnt) break;
+      rem -= cnt;
+    }
+    r = max(0, d - (G - 1)) + rem;
+    cc = d - r;
+  }
+  const int tile = r * G + cc;
   const int j0 = r * N;
   const int k0 = cc * N;
-  const int left = cc ? t - 1 : T;
-  const int up = r ? t - G : T;
+  const int left = cc ? tile - 1 : T;
+  const int up = r ? tile - G : T;
   const int skew = r + cc;
   const int g2 = args.g2;
   const int ag2 = -g2;
+  auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
   for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
 
-  // ---- per-lane stream state ---------------------------------------------
-  int item[LANES], iend[LANES], tid[LANES], si[LANES], la[LANES], lb[LANES], lc[LANES];
-  uint32_t w0[LANES], s0word[LANES];
-  bool done[LANES];
-  int bestv[LANES];
-  uint32_t bestlin[LANES];
-  bool bestok[LANES];
+  // hot per-lane state in registers
+  int si[LANES], la[LANES];
+  uint32_t s0word[LANES], flags[LANES];
 
-  // Builds this thread's sigma tables for lane l (triplet id, or -1 = null
-  // lane with all-zero weights, which keeps an idle lane bounded).
+  // 2-bit codes of the N bases at positions [pos, pos + N) of a sequence of
+  // length len (packed at word w), slot s -> bits 2s; out of range -> 0.
+  auto load_codes = [&](uint32_t w, int pos, int len) -> uint32_t {
+    const int p0 = pos < 0 ? 0 : pos;
+    if (p0 >= len) return 0u;
+    const uint32_t* src = args.seq + w + (p0 >> 4);
+    const unsigned long long both =
+        static_cast<unsigned long long>(__ldg(src)) | (static_cast<unsigned long long>(__ldg(src + 1)) << 32);
+    uint32_t codes = static_cast<uint32_t>(both >> (2 * (p0 & 15)));
+    if (pos < 0) codes <<= 2;
+    const int nvalid = len - pos;
+    if (nvalid < 16) codes &= (1u << (2 * nvalid)) - 1u;
+    return codes;
+  };
+
+  // Loads triplet `id` (or the null triplet, id < 0: all-zero weights, which
+  // keeps an idle lane's values bounded) into lane l of this thread: sigma
+  // tables in shared memory, lengths, flags.
   auto setup = [&](int l, int id) {
     int a_ = 0x3FFFFFFF, b_ = -1, c_ = -1;
-    uint32_t ww1 = 0, ww2 = 0;
+    uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
     if (id >= 0) {
-      const TripletDesc d = args.desc[id];
-      a_ = d.a;
-      b_ = d.b;
-      c_ = d.c;
-      w0[l] = d.w0;
-      ww1 = d.w1;
-      ww2 = d.w2;
+      const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(args.desc + id));
+      const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(args.desc + id) + 1);
+      a_ = static_cast<int>(d0.x);
+      b_ = static_cast<int>(d0.y);
+      c_ = static_cast<int>(d0.z);
+      ww0 = d1.x;
+      ww1 = d1.y;
+      ww2 = d1.z;
     }
     la[l] = a_;
-    lb[l] = b_;
-    lc[l] = c_;
+    LS(l, kTid) = id;
+    LS(l, kLenB) = b_;
+    LS(l, kLenC) = c_;
+    LS(l, kW0) = static_cast<int32_t>(ww0);
+    uint32_t f = id >= 0 ? 0u : kDone;
+    if (id >= 0 && b_ / N == r && c_ / N == cc) f |= kOwner;
+    flags[l] = f;
     const int mp = id >= 0 ? args.match_p : 0;
     const int mm = id >= 0 ? args.mismatch_p : 0;
-    int x1[N], x2[N];
+    const uint32_t c1 = load_codes(ww1, j0 - 1, b_);
+    const uint32_t c2 = load_codes(ww2, k0 - 1, c_);
+    if constexpr (LANES == 1) {
+      // int16 tables: 4 values (s0 code 0..3) per row, 8 B per (row, thread)
 #pragma unroll
-    for (int p = 0; p < N; ++p) x1[p] = base_at(args.seq, ww1, j0 + p - 1, b_);
+      for (int p = 0; p < N; ++p) {
+        const uint32_t x1 = (c1 >> (2 * p)) & 3u, x2 = (c2 >> (2 * p)) & 3u;
+        uint32_t v1[4], v2[4];
 #pragma unroll
-    for (int q = 0; q < N; ++q) x2[q] = base_at(args.seq, ww2, k0 + q - 1, c_);
-#pragma unroll
-    for (int p = 0; p < N; ++p) {
-#pragma unroll
-      for (int code = 0; code < 4; ++code) {
-        const int v1 = code == x1[p] ? mp : mm;
-        const int v2 = code == x2[p] ? mp : mm;
-        if constexpr (LANES == 1) {
-          reinterpret_cast<int16_t*>(tab1)[(p * 4 + code) * T + t] = static_cast<int16_t>(v1);
-          reinterpret_cast<int16_t*>(tab2)[(p * 4 + code) * T + t] = static_cast<int16_t>(v2);
-        } else {
-          tab1[(size_t(p) * T + t) * 8 + l * 4 + code] = static_cast<unsigned char>(v1);
-          tab2[(size_t(p) * T + t) * 8 + l * 4 + code] = static_cast<unsigned char>(v2);
+        for (int code = 0; code < 4; ++code) {
+          v1[code] = static_cast<uint32_t>(code == int(x1) ? mp : mm) & 0xFFFFu;
+          v2[code] = static_cast<uint32_t>(code == int(x2) ? mp : mm) & 0xFFFFu;
         }
+        reinterpret_cast<uint2*>(tab1)[p * T + t] = make_uint2(v1[0] | (v1[1] << 16), v1[2] | (v1[3] << 16));
+        reinterpret_cast<uint2*>(tab2)[p * T + t] = make_uint2(v2[0] | (v2[1] << 16), v2[2] | (v2[3] << 16));
       }
-    }
+      const int sc = TRACE ? 16 : 1;
+      const int tg = TRACE ? static_cast<int>(kTagT4) : 0;
 #pragma unroll
-    for (int p = 0; p < N; ++p) {
+      for (int g = 0; g < NN / 4; ++g) {
+        uint32_t v[4];
 #pragma unroll
-      for (int q = 0; q < N; ++q) {
-        const int cell = p * N + q;
-        const int v = x1[p] == x2[q] ? mp : mm;
-        const size_t word = size_t(cell >> 2) * T * 4 + size_t(t) * 4 + (cell & 3);
-        if constexpr (LANES == 1) {
-          s12w[word] = static_cast<uint32_t>(TRACE ? (v * 16 + static_cast<int>(kTagT4)) : v);
-        } else {
-          reinterpret_cast<uint16_t*>(s12w)[word * 2 + l] = static_cast<uint16_t>(v);
+        for (int e = 0; e < 4; ++e) {
+          const int cell = g * 4 + e, p = cell / N, q = cell % N;
+          v[e] = static_cast<uint32_t>((((c1 >> (2 * p)) & 3u) == ((c2 >> (2 * q)) & 3u) ? mp : mm) * sc + tg);
+        }
+        s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
+      }
+    } else {
+      // byte tables: sigma'(code, x) = mm + (mp - mm) * [code == x], byte `code`
+      const uint32_t mm8 = static_cast<uint32_t>(mm) * 0x01010101u;
+      const uint32_t dm = static_cast<uint32_t>(mp - mm);
+      uint32_t t2w[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const uint32_t x1 = (c1 >> (2 * p)) & 3u, x2 = (c2 >> (2 * p)) & 3u;
+        reinterpret_cast<uint32_t*>(tab1)[(p * T + t) * 2 + l] = mm8 + (dm << (8 * x1));
+        t2w[p] = mm8 + (dm << (8 * x2));
+        reinterpret_cast<uint32_t*>(tab2)[(p * T + t) * 2 + l] = t2w[p];
+      }
+      uint16_t* s12h = reinterpret_cast<uint16_t*>(s12w);
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        const uint32_t x1 = (c1 >> (2 * p)) & 3u;
+        const uint32_t sel = x1 | ((x1 | 8u) << 4);
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          const int cell = p * N + q;
+          s12h[((size_t(cell >> 2) * T + t) * 4 + (cell & 3)) * 2 + l] = static_cast<uint16_t>(prmt(t2w[q], 0u, sel));
         }
       }
     }
@@ -231,23 +290,15 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   const int sbase = blockIdx.x * LANES;
 #pragma unroll
   for (int l = 0; l < LANES; ++l) {
-    item[l] = args.stream_off[sbase + l];
-    iend[l] = args.stream_off[sbase + l + 1];
+    const int it = args.stream_off[sbase + l];
+    const int ie = args.stream_off[sbase + l + 1];
+    LS(l, kItem) = it;
+    LS(l, kIEnd) = ie;
+    LS(l, kBestV) = 0;
+    LS(l, kBestLin) = 0;
     si[l] = 0;
-    bestok[l] = false;
-    bestv[l] = 0;
-    bestlin[l] = 0;
     s0word[l] = 0;
-    w0[l] = 0;
-    if (item[l] < iend[l]) {
-      tid[l] = args.items[item[l]];
-      done[l] = false;
-      setup(l, tid[l]);
-    } else {
-      tid[l] = -1;
-      done[l] = true;
-      setup(l, -1);
-    }
+    setup(l, it < ie ? args.items[it] : -1);
   }
 
   uint32_t Pv[N + 1][N + 1];
@@ -256,15 +307,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
     for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = NEG;
 
-  // column constants
-  uint32_t colc[N];   // local floor: |g2| * (Q-1)        (x 2^SH)
-  uint32_t cold[N];   // best tracking: g2 * (Q-1)       (x 2^SH)
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    colc[q] = Ops::splat((ag2 * q) << SH);
-    cold[q] = Ops::splat((g2 * q) << SH);
-  }
-
   __syncthreads();
 
   const int nsteps = args.cta_steps[blockIdx.x];
@@ -272,9 +314,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     const int buf = s & 1;
     bool any = false;
 #pragma unroll
-    for (int l = 0; l < LANES; ++l) any |= !done[l];
+    for (int l = 0; l < LANES; ++l) any |= !(flags[l] & kDone);
     if (s >= skew && any) {
-      // ---- 1. new halos (published by neighbours at step s-1) ----------
+      // ---- 1. new halos (published by the neighbours at step s-1) --------
       uint32_t Cu[N + 1][N + 1];
       const uint32_t* xin = xbuf + (buf ^ 1) * XW * (T + 1);
 #pragma unroll
@@ -282,87 +324,62 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
       for (int p = 0; p < N; ++p) Cu[p + 1][0] = xin[p * (T + 1) + left];
 
-      // ---- 2. per-slice sigma rows/cols ---------------------------------
-      int code[LANES];
+      // ---- 2. per-slice sigma row / column tables -----------------------
+      uint32_t sel = 0;  // LANES == 2: PRMT selector; LANES == 1: code
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
-        const int i = si[l];
-        code[l] = 0;
-        if (i >= 1 && !done[l]) {
-          const int pos = i - 1;
-          if ((pos & 15) == 0) s0word[l] = __ldg(args.seq + w0[l] + (pos >> 4));
-          code[l] = static_cast<int>((s0word[l] >> ((pos & 15) * 2)) & 3u);
+        const int pos = si[l] - 1;
+        const uint32_t code = pos >= 0 ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
+        if constexpr (LANES == 1) {
+          sel = code;
+        } else {
+          const uint32_t b = code + 4u * l;
+          sel |= (b | ((b | 8u) << 4)) << (8 * l);
         }
       }
-      uint32_t s01[N], s02[N];
-      if constexpr (LANES == 1) {
-        const int16_t* t1 = reinterpret_cast<const int16_t*>(tab1) + code[0] * T + t;
-        const int16_t* t2 = reinterpret_cast<const int16_t*>(tab2) + code[0] * T + t;
-#pragma unroll
-        for (int p = 0; p < N; ++p) {
-          const int v1 = t1[p * 4 * T];
-          const int v2 = t2[p * 4 * T];
-          if constexpr (TRACE) {
-            s01[p] = static_cast<uint32_t>(v1 * 16 + static_cast<int>(kTagT2));
-            s02[p] = static_cast<uint32_t>(v2 * 16 + static_cast<int>(kTagT3));
-          } else {
-            s01[p] = static_cast<uint32_t>(v1);
-            s02[p] = static_cast<uint32_t>(v2);
-          }
+      auto sig_row = [&](const unsigned char* tab, int p) -> uint32_t {
+        if constexpr (LANES == 1) {
+          return static_cast<uint32_t>(static_cast<int>(
+              reinterpret_cast<const int16_t*>(tab)[(size_t(p) * T + t) * 4 + sel]));
+        } else {
+          const uint2 e = reinterpret_cast<const uint2*>(tab)[p * T + t];
+          return prmt(e.x, e.y, sel);
         }
-      } else {
-        const uint32_t c0 = static_cast<uint32_t>(code[0]);
-        const uint32_t c1 = static_cast<uint32_t>(code[1]) + 4u;
-        const uint32_t sel = c0 | ((c0 | 8u) << 4) | (c1 << 8) | ((c1 | 8u) << 12);
-        const uint2* t1 = reinterpret_cast<const uint2*>(tab1) + t;
-        const uint2* t2 = reinterpret_cast<const uint2*>(tab2) + t;
+      };
+      uint32_t s02[N];
 #pragma unroll
-        for (int p = 0; p < N; ++p) {
-          const uint2 e1 = t1[p * T];
-          const uint2 e2 = t2[p * T];
-          s01[p] = prmt(e1.x, e1.y, sel);
-          s02[p] = prmt(e2.x, e2.y, sel);
-        }
+      for (int q = 0; q < N; ++q) {
+        s02[q] = sig_row(tab2, q);
+        if constexpr (TRACE) s02[q] = s02[q] * 16u + kTagT3;
       }
 
       // ---- 3. forced cells (reference initialisation, oracle.cpp:30-39) --
       // global: M(0,0,0) = 0; semi: axis cells are 0 in M-space.
       uint32_t fcorner = NEG;
-      uint32_t frow[N], fcol[N];  // semi slice-0 faces (row j=0 / col k=0)
-      bool semi0 = false;
-#pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        const bool live = !done[l];
-        if constexpr (MODE == kGlobal) {
-          if (t == 0 && live && si[l] == 0) fcorner = lop_sel(fcorner, 0u, Ops::mask(l));
-        } else if constexpr (MODE == kSemi) {
-          if (t == 0 && live)
-            fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
-          semi0 |= live && si[l] == 0 && (r == 0 || cc == 0);
-        }
-      }
+      uint32_t frow[MODE == kSemi ? N : 1], fcol[MODE == kSemi ? N : 1];
+      uint32_t flbase = 0;
       if constexpr (MODE == kSemi) {
 #pragma unroll
         for (int q = 0; q < N; ++q) frow[q] = fcol[q] = NEG;
-        if (semi0) {
+      }
 #pragma unroll
-          for (int l = 0; l < LANES; ++l) {
-            if (!done[l] && si[l] == 0) {
+      for (int l = 0; l < LANES; ++l) {
+        const bool live = !(flags[l] & kDone);
+        if constexpr (MODE == kGlobal) {
+          if (t == 0 && live && si[l] == 0) fcorner = lop_sel(fcorner, 0u, Ops::mask(l));
+        } else if constexpr (MODE == kSemi) {
+          if (t == 0 && live) fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
+          if (live && si[l] == 0 && (r == 0 || cc == 0)) {
 #pragma unroll
-              for (int q = 0; q < N; ++q) {
-                if (r == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (k0 + q)) << SH), Ops::mask(l));
-                if (cc == 0) fcol[q] = lop_sel(fcol[q], Ops::splat((ag2 * (j0 + q)) << SH), Ops::mask(l));
-              }
+            for (int q = 0; q < N; ++q) {
+              if (r == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (k0 + q)) << SH), Ops::mask(l));
+              if (cc == 0) fcol[q] = lop_sel(fcol[q], Ops::splat((ag2 * (j0 + q)) << SH), Ops::mask(l));
             }
           }
-        }
-      }
-      // local floor base per lane: |g2| * (i + j0 + k0)
-      uint32_t flbase = 0;
-      if constexpr (MODE == kLocal) {
-#pragma unroll
-        for (int l = 0; l < LANES; ++l)
+        } else {
+          // local floor base: |g2| * (i + j0 + k0)
           flbase = lop_sel(flbase, Ops::splat((ag2 * (si[l] + j0 + k0)) << SH), Ops::mask(l));
+        }
       }
 
       // ---- 4. the tile: 6 integer instructions per cell -----------------
@@ -375,16 +392,15 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       uint4 sg4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int P = 1; P <= N; ++P) {
+        uint32_t a1 = sig_row(tab1, P - 1);
+        if constexpr (TRACE) a1 = a1 * 16u + kTagT2;
         uint32_t flrow = 0;
-        if constexpr (MODE == kLocal) {
-          flrow = flbase + Ops::splat((ag2 * (P - 1)) << SH) + (TRACE ? kTagStop : 0u);
-        }
+        if constexpr (MODE == kLocal) flrow = flbase + Ops::splat((ag2 * (P - 1)) << SH) + (TRACE ? kTagStop : 0u);
 #pragma unroll
         for (int Q = 1; Q <= N; ++Q) {
           const int cell = (P - 1) * N + (Q - 1);
           if ((cell & 3) == 0) sg4 = s12v[(cell >> 2) * T + t];
           const uint32_t sg = (cell & 3) == 0 ? sg4.x : (cell & 3) == 1 ? sg4.y : (cell & 3) == 2 ? sg4.z : sg4.w;
-          const uint32_t a1 = s01[P - 1];
           const uint32_t a2 = s02[Q - 1];
           uint32_t x;
           if constexpr (!TRACE) {
@@ -404,7 +420,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::addmax(Pv[P][Q], kTagT5, x);                    // t5
             x = Ops::addmax(Cu[P - 1][Q], kTagT6, x);                // t6
           }
-          if constexpr (MODE == kLocal) x = Ops::addmax(flrow, colc[Q - 1], x);  // floor 0
+          if constexpr (MODE == kLocal) x = Ops::addmax(flrow, Ops::splat((ag2 * (Q - 1)) << SH), x);  // floor 0
           if constexpr (MODE == kGlobal || MODE == kSemi) {
             if (P == 1 && Q == 1) x = Ops::max2(x, fcorner);
           }
@@ -421,7 +437,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       }
 
       // ---- 5. publish right column / down row (+ corner) ----------------
-      uint32_t* xout = xbuf + buf * XW * (T + 1) + t;
+      uint32_t* xout = xbuf + buf * XW * (T + 1) + tile;
 #pragma unroll
       for (int p = 0; p < N; ++p) xout[p * (T + 1)] = Cu[p + 1][N];
 #pragma unroll
@@ -429,8 +445,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
       // ---- 6. direction cube slot (64 B per tile-slice) -----------------
       if constexpr (TRACE) {
-        if (!done[0]) {
-          uint4* dst = args.dirs + args.dir_off[tid[0]] + (size_t(si[0]) * T + t) * 4;
+        if (!(flags[0] & kDone)) {
+          uint4* dst = args.dirs + args.dir_off[LS(0, kTid)] + (size_t(si[0]) * T + tile) * 4;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             if (v * 4 < NW) {
@@ -443,67 +459,50 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       }
 
       // ---- 7. score extraction ------------------------------------------
+      if constexpr (MODE == kGlobal) {
+        // M[a, b, c] (tiled.hpp:495-502): the owner tile, last slice
 #pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        if (done[l]) continue;
-        const int i = si[l];
-        if constexpr (MODE == kGlobal) {
-          // reads M[a, b, c] (tiled.hpp:495-502): the owner tile, last slice
-          if (i == la[l] && (lb[l] / N) == r && (lc[l] / N) == cc) {
-            const int want = (lb[l] - j0 + 1) * (N + 1) + (lc[l] - k0 + 1);
+        for (int l = 0; l < LANES; ++l) {
+          if ((flags[l] & kOwner) && si[l] == la[l]) {
+            const int B = LS(l, kLenB), C = LS(l, kLenC), id = LS(l, kTid);
+            const int want = (B - j0 + 1) * (N + 1) + (C - k0 + 1);
             uint32_t v = 0;
 #pragma unroll
             for (int P = 1; P <= N; ++P)
 #pragma unroll
               for (int Q = 1; Q <= N; ++Q)
                 if (P * (N + 1) + Q == want) v = Cu[P][Q];
-            const int mv = Ops::lane(v, l) >> SH;
-            const int id = tid[l];
-            args.out_score[id] = mv + g2 * (la[l] + lb[l] + lc[l]);
+            args.out_score[id] = (Ops::lane(v, l) >> SH) + g2 * (la[l] + B + C);
             args.out_end[3 * id] = la[l];
-            args.out_end[3 * id + 1] = lb[l];
-            args.out_end[3 * id + 2] = lc[l];
+            args.out_end[3 * id + 1] = B;
+            args.out_end[3 * id + 2] = C;
           }
         }
-      }
-      if constexpr (MODE != kGlobal) {
-        // Best tracking (oracle.cpp:67-88, tiled.hpp:129-144, 222-228):
-        // max value, ties to the lexicographically smallest (i, j, k).
-        // Candidates: local = every real cell; semi = cells with
-        // i == a || j == b || k == c.  Non-candidates are masked out.
-        uint32_t rin[N], cin[N], rf[N], cf[N];
-        bool cand[LANES];
+      } else {
+        // Best tracking (oracle.cpp:67-88, tiled.hpp:129-144, 222-228): max
+        // value, ties to the lexicographically smallest (i, j, k).
+        // Candidates: local = every real cell; semi = i == a || j == b || k == c.
+        int rb[LANES], cb[LANES];
+        bool cand[LANES], last[LANES];
         bool anyc = false;
 #pragma unroll
-        for (int p = 0; p < N; ++p) rin[p] = cin[p] = rf[p] = cf[p] = 0;
-#pragma unroll
         for (int l = 0; l < LANES; ++l) {
-          cand[l] = false;
-          if (done[l]) continue;
-          const bool lastslice = si[l] == la[l];
-#pragma unroll
-          for (int p = 0; p < N; ++p) {
-            const int j = j0 + p, k = k0 + p;
-            if (j <= lb[l]) rin[p] |= Ops::mask(l);
-            if (k <= lc[l]) cin[p] |= Ops::mask(l);
-            if (MODE == kSemi && (j == lb[l] || lastslice)) rf[p] |= Ops::mask(l);
-            if (MODE == kSemi && k == lc[l]) cf[p] |= Ops::mask(l);
-          }
-          const bool inside = j0 <= lb[l] && k0 <= lc[l];
-          if (MODE == kLocal) {
-            cand[l] = inside;
-          } else {
-            cand[l] = inside && (lastslice || (lb[l] - j0) < N || (lc[l] - k0) < N);
-          }
+          rb[l] = LS(l, kLenB) - j0;  // rows P-1 <= rb are real
+          cb[l] = LS(l, kLenC) - k0;
+          last[l] = si[l] == la[l];
+          const bool inside = !(flags[l] & kDone) && rb[l] >= 0 && cb[l] >= 0;
+          cand[l] = MODE == kLocal ? inside : inside && (last[l] || rb[l] < N || cb[l] < N);
           anyc |= cand[l];
         }
-        auto masked = [&](int P, int Q) -> uint32_t {
-          if constexpr (MODE == kLocal) {
-            return Cu[P][Q] & rin[P - 1] & cin[Q - 1];
-          } else {
-            const uint32_t keep = (rf[P - 1] & rin[P - 1] & cin[Q - 1]) | (rin[P - 1] & cf[Q - 1]);
-            return lop_sel(NEG, Cu[P][Q], keep);
+        auto keep_mask = [&](int P, int Q) -> uint32_t {
+          uint32_t m = 0;
+#pragma unroll
+          for (int l = 0; l < LANES; ++l) {
+            const bool in = cand[l] && P - 1 <= rb[l] && Q - 1 <= cb[l];
+            const bool face = MODE == kLocal || last[l] || P - 1 == rb[l] || Q - 1 == cb[l];
+            if (in && face) m |= Ops::mask(l);
           }
+          return m;
         };
         if (anyc) {
           uint32_t stepmax = NEG;
@@ -511,16 +510,16 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           for (int P = 1; P <= N; ++P) {
             uint32_t rowacc = NEG;
 #pragma unroll
-            for (int Q = 1; Q <= N; ++Q) rowacc = Ops::addmax(masked(P, Q), cold[Q - 1], rowacc);
+            for (int Q = 1; Q <= N; ++Q)
+              rowacc = Ops::addmax(lop_sel(NEG, Cu[P][Q], keep_mask(P, Q)), Ops::splat((g2 * (Q - 1)) << SH), rowacc);
             stepmax = Ops::addmax(rowacc, Ops::splat((g2 * (P - 1)) << SH), stepmax);
           }
 #pragma unroll
           for (int l = 0; l < LANES; ++l) {
             if (!cand[l]) continue;
             const int sm = Ops::lane(stepmax, l);
-            const int base = (g2 * (si[l] + j0 + k0)) << SH;
-            const int mval = (sm + base) >> SH;
-            if (!bestok[l] || mval > bestv[l]) {
+            const int mval = (sm + ((g2 * (si[l] + j0 + k0)) << SH)) >> SH;
+            if (!(flags[l] & kBestOk) || mval > LS(l, kBestV)) {
               // first cell (row-major = lexicographic) attaining the maximum
               int fp = 0, fq = 0;
               bool found = false;
@@ -528,7 +527,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               for (int P = 1; P <= N; ++P)
 #pragma unroll
                 for (int Q = 1; Q <= N; ++Q) {
-                  const int v = Ops::lane(masked(P, Q), l) + ((g2 * (P - 1 + Q - 1)) << SH);
+                  const int v = Ops::lane(lop_sel(NEG, Cu[P][Q], keep_mask(P, Q)), l) + ((g2 * (P - 1 + Q - 1)) << SH);
                   if (!found && v == sm) {
                     found = true;
                     fp = P - 1;
@@ -536,10 +535,11 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
                   }
                 }
               const uint32_t j = j0 + fp, k = k0 + fq;
-              bestv[l] = mval;
-              bestlin[l] = (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(lb[l] + 1) + j) *
-                               static_cast<uint32_t>(lc[l] + 1) + k;
-              bestok[l] = true;
+              LS(l, kBestV) = mval;
+              LS(l, kBestLin) = static_cast<int32_t>(
+                  (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
+                      static_cast<uint32_t>(LS(l, kLenC) + 1) + k);
+              flags[l] |= kBestOk;
             }
           }
         }
@@ -551,29 +551,23 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
         for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = Cu[P][Q];
 
-      // ---- 9. advance the lanes -----------------------------------------
+      // ---- 9. advance the lanes (switch triplets at the end of a stream item)
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
-        if (done[l]) continue;
+        if (flags[l] & kDone) continue;
         si[l] += 1;
         if (si[l] > la[l]) {
           if constexpr (MODE != kGlobal) {
-            if (bestok[l]) {
+            if (flags[l] & kBestOk) {
               const unsigned long long key =
-                  (static_cast<unsigned long long>(static_cast<uint32_t>(bestv[l]) ^ 0x80000000u) << 32) |
-                  static_cast<unsigned long long>(0xFFFFFFFFu - bestlin[l]);
-              atomicMax(args.out_key + tid[l], key);
+                  (static_cast<unsigned long long>(static_cast<uint32_t>(LS(l, kBestV)) ^ 0x80000000u) << 32) |
+                  static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(LS(l, kBestLin)));
+              atomicMax(args.out_key + LS(l, kTid), key);
             }
-            bestok[l] = false;
           }
-          item[l] += 1;
-          if (item[l] < iend[l]) {
-            tid[l] = args.items[item[l]];
-            setup(l, tid[l]);
-          } else {
-            done[l] = true;
-            setup(l, -1);
-          }
+          const int it = LS(l, kItem) + 1;
+          LS(l, kItem) = it;
+          setup(l, it < LS(l, kIEnd) ? args.items[it] : -1);
           si[l] = 0;
 #pragma unroll
           for (int P = 0; P <= N; ++P)
@@ -581,6 +575,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = lop_sel(Pv[P][Q], NEG, Ops::mask(l));
         }
       }
+    }
+    // next slice's s0 word (consumed after the barrier: latency hidden)
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) {
+      const int pos = si[l] - 1;
+      s0word[l] = (!(flags[l] & kDone) && pos >= 0) ? __ldg(args.seq + static_cast<uint32_t>(LS(l, kW0)) + (pos >> 4)) : 0u;
     }
     __syncthreads();
   }
