@@ -66,7 +66,10 @@ struct BucketLaunch {
   int grid = 0, lanes = 0, mode = 0;
   ta::KernelEntry ke;
   int ctas = 0;
-  DevBuf<int32_t> items, soff, steps;
+  DevBuf<int4> items;
+  DevBuf<int32_t> soff, steps;
+  DevBuf<int32_t> faces;
+  DevBuf<int64_t> face_off;
   int64_t padded = 0;
 };
 
@@ -151,10 +154,14 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
   constexpr int N = ta::kTileN;
   const int T = grid * grid;
   const uint32_t* base = dirs + dir_off[id] * 4;
+  const int GN = grid * N;
+  const int Bk = (d.c + 1 + GN - 1) / GN;
   auto code_at = [&](int i, int j, int k) -> uint32_t {
-    const int t = (j / N) * grid + (k / N);
-    const int cell = (j % N) * N + (k % N);
-    const uint32_t w = base[(int64_t(i) * T + t) * 16 + (cell >> 3)];
+    const int blk = (j / GN) * Bk + (k / GN);
+    const int jj = j % GN, kk = k % GN;
+    const int t = (jj / N) * grid + (kk / N);
+    const int cell = (jj % N) * N + (kk % N);
+    const uint32_t w = base[((int64_t(blk) * (d.a + 1) + i) * T + t) * 16 + (cell >> 3)];
     return (w >> ((cell & 7) * 4)) & 15u;
   };
   auto stop_at = [&](int i, int j, int k, uint32_t code) {
@@ -304,21 +311,31 @@ struct LanePlan {
   bool packed16 = false;
 };
 
-bool s16_ok(const ta_scheme& s, int max_a, int grid) {
+// Largest in-grid cell value (gap-shifted, >= 0) a triplet can produce, incl.
+// padding cells and idle slices: (match + |g2|) * (slices + j extent + k extent).
+int64_t lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c, int grid) {
   const int g2 = 2 * s.gap;
-  const int mp = s.match - g2, mm = s.mismatch - g2;
-  if (mm < 0 || mp > 127) return false;  // carry-free IADD3 + byte tables
-  const int64_t ext = int64_t(grid) * ta::kTileN;
-  const int64_t bound = int64_t(s.match - g2) * (int64_t(max_a) + 2 * ext) + 3 * 127 +
-                        int64_t(-g2) * 2 * ta::kTileN;
-  return bound <= 16000;
+  const int64_t gn = int64_t(grid) * ta::kTileN;
+  const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
+  const int64_t slices = std::max<int64_t>(a + 1, grid + 1);
+  return int64_t(s.match - g2) * (slices + ej + ek);
 }
 
+bool s16_ok(const ta_scheme& s, int64_t max_bound) {
+  const int g2 = 2 * s.gap;
+  const int mp = s.match - g2, mm = s.mismatch - g2;
+  if (mm < 0 || mp > 127) return false;  // carry-free packed adds + byte tables
+  // values in [0, bound]; unreachable terms stay below 0 from NEG = -16384
+  return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kTileN <= 32000;
+}
+
+// Smallest tile grid whose plane holds the triplet; longer triplets use the
+// largest grid as a sequence of blocks.
 int pick_grid(int32_t b, int32_t c) {
   const int ext = std::max(b, c) + 1;
   for (int g : ta::kGridSizes)
     if (g * ta::kTileN >= ext) return g;
-  return -1;
+  return ta::kGridSizes[ta::kNumGrid - 1];
 }
 
 }  // namespace
@@ -359,33 +376,71 @@ struct ta_batch {
 namespace {
 
 struct StreamPlan {
-  std::vector<int32_t> items, soff, steps;
+  std::vector<int4> items;
+  std::vector<int32_t> soff, steps;
+  std::vector<int64_t> face_off;
+  int64_t face_words = 0;
+  int64_t padded_slices = 0;  // sum over items of slices * blocks (for stats)
 };
 
+struct Blocks {
+  int bj = 1, bk = 1;
+};
+
+inline Blocks blocks_of(int32_t b, int32_t c, int grid) {
+  const int gn = grid * ta::kTileN;
+  return Blocks{(b + 1 + gn - 1) / gn, (c + 1 + gn - 1) / gn};
+}
+
+// slices one block item occupies in a stream: a+1, padded to >= G+1 for
+// multi-block triplets so a block's faces are written >= 2 steps before the
+// next block's edge tiles prefetch them.
+inline int item_len(int32_t a, const Blocks& bl, int grid) {
+  return (bl.bj * bl.bk > 1) ? std::max(a + 1, grid + 1) : a + 1;
+}
+
 // Greedy least-loaded assignment of triplets to CTA lane streams (the
-// "dynamic" rule of plan_partition, dispatch.cpp:46-56, applied to slices).
-void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, int ctas,
-                  int lanes, int grid, StreamPlan* out) {
+// "dynamic" rule of plan_partition, dispatch.cpp:46-56, applied to slices);
+// a long triplet contributes its Bj*Bk blocks as consecutive items.
+void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a,
+                  const std::vector<int32_t>& b, const std::vector<int32_t>& c, int ctas, int lanes, int grid,
+                  StreamPlan* out) {
   const int S = ctas * lanes;
+  const int gn = grid * ta::kTileN;
   std::vector<std::vector<int32_t>> lists(static_cast<size_t>(S));
   using Load = std::pair<int64_t, int32_t>;
   std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
   for (int s = 0; s < S; ++s) heap.push({0, s});
-  std::vector<int64_t> load(static_cast<size_t>(S), 0);
+  std::vector<int64_t> load(static_cast<size_t>(S), 0), face(static_cast<size_t>(S), 0);
   for (int32_t id : ids) {
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+    const int64_t len = item_len(a[size_t(id)], bl, grid);
     Load top = heap.top();
     heap.pop();
     lists[size_t(top.second)].push_back(id);
-    top.first += a[size_t(id)] + 1;
+    top.first += len * bl.bj * bl.bk;
     load[size_t(top.second)] = top.first;
+    if (bl.bj * bl.bk > 1)
+      face[size_t(top.second)] = std::max(face[size_t(top.second)], ta::face_words(a[size_t(id)], bl.bk, gn));
     heap.push(top);
   }
   out->items.clear();
   out->soff.assign(size_t(S) + 1, 0);
   out->steps.assign(size_t(ctas), 0);
+  out->face_off.assign(size_t(S), 0);
+  out->face_words = 0;
+  out->padded_slices = 0;
   for (int s = 0; s < S; ++s) {
     out->soff[size_t(s)] = int32_t(out->items.size());
-    out->items.insert(out->items.end(), lists[size_t(s)].begin(), lists[size_t(s)].end());
+    out->face_off[size_t(s)] = out->face_words;
+    out->face_words += face[size_t(s)];
+    for (int32_t id : lists[size_t(s)]) {
+      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+      const int len = item_len(a[size_t(id)], bl, grid);
+      for (int J = 0; J < bl.bj; ++J)
+        for (int K = 0; K < bl.bk; ++K) out->items.push_back(make_int4(id, (J << 16) | K, len, (bl.bj << 16) | bl.bk));
+      out->padded_slices += int64_t(len) * bl.bj * bl.bk;
+    }
   }
   out->soff[size_t(S)] = int32_t(out->items.size());
   for (int cta = 0; cta < ctas; ++cta) {
@@ -401,7 +456,15 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   bl->grid = grid;
   bl->lanes = lanes;
   bl->mode = mode;
-  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace);
+  bool multi = false;
+  for (int32_t id : ids) {
+    const Blocks b = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], grid);
+    if (b.bj * b.bk > 1) {
+      multi = true;
+      break;
+    }
+  }
+  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, multi);
   const ta::KernelEntry& ke = bl->ke;
   if (!ke.fn) return fail(TA_ERR_LOGIC, "no kernel instantiation for grid " + std::to_string(grid));
   TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
@@ -411,15 +474,18 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
   bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
   StreamPlan plan;
-  plan_streams(ids, bt->a, bl->ctas, lanes, grid, &plan);
+  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, grid, &plan);
+  if (plan.face_words > (int64_t(1) << 31)) return fail(TA_ERR_CAPACITY, "block-face scratch exceeds 2^31 words");
   TA_CK(bl->items.reserve(plan.items.size()));
   TA_CK(bl->soff.reserve(plan.soff.size()));
   TA_CK(bl->steps.reserve(plan.steps.size()));
-  TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * 4, cudaMemcpyHostToDevice, st));
+  TA_CK(bl->faces.reserve(size_t(plan.face_words) + 1));
+  TA_CK(bl->face_off.reserve(plan.face_off.size()));
+  TA_CK(cudaMemcpyAsync(bl->face_off.ptr, plan.face_off.data(), plan.face_off.size() * 8, cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
-  bl->padded = 0;
-  for (int32_t id : ids) bl->padded += int64_t(bt->a[size_t(id)] + 1) * grid * grid * ta::kTileN * ta::kTileN;
+  bl->padded = plan.padded_slices * grid * grid * ta::kTileN * ta::kTileN;
   return TA_OK;
 }
 
@@ -428,6 +494,8 @@ int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st,
   args.items = bl->items.ptr;
   args.stream_off = bl->soff.ptr;
   args.cta_steps = bl->steps.ptr;
+  args.faces = bl->faces.ptr;
+  args.face_off = bl->face_off.ptr;
   bl->ke.fn<<<bl->ctas, bl->ke.threads, bl->ke.smem, st>>>(args);
   TA_CK(cudaGetLastError());
   *launches += 1;
@@ -460,7 +528,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   std::vector<std::vector<int32_t>> buckets(ta::kNumGrid);
   std::vector<int32_t> all_ok;
   all_ok.reserve(size_t(n));
-  int max_a_bucket[ta::kNumGrid] = {0};
+  int64_t max_bound_bucket[ta::kNumGrid] = {0};
   for (int64_t t = 0; t < n; ++t) {
     if (bt->status[size_t(t)] != TA_OK) continue;
     const int32_t A = bt->a[size_t(t)], B = bt->b[size_t(t)], C = bt->c[size_t(t)];
@@ -491,14 +559,10 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       continue;
     }
     const int g = pick_grid(B, C);
-    if (g < 0) {
-      bt->status[size_t(t)] = TA_ERR_CAPACITY;  // long-triplet path not built yet
-      continue;
-    }
     int gi = 0;
     while (ta::kGridSizes[gi] != g) ++gi;
     buckets[size_t(gi)].push_back(int32_t(t));
-    max_a_bucket[gi] = std::max(max_a_bucket[gi], A);
+    max_bound_bucket[gi] = std::max(max_bound_bucket[gi], lane_bound(scheme, A, B, C, g));
     all_ok.push_back(int32_t(t));
   }
   if (cfg_rc) g_err = cfg_msg;
@@ -512,6 +576,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   base.g2 = 2 * scheme.gap;
   base.match_p = scheme.match - base.g2;
   base.mismatch_p = scheme.mismatch - base.g2;
+  base.one = 1u;
 
   if (!bt->ev0) TA_CK(cudaEventCreate(&bt->ev0));
   if (!bt->ev1) TA_CK(cudaEventCreate(&bt->ev1));
@@ -527,7 +592,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     std::vector<int> lanes_of(ta::kNumGrid, 1);
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       if (buckets[size_t(gi)].empty()) continue;
-      lanes_of[size_t(gi)] = s16_ok(scheme, max_a_bucket[gi], ta::kGridSizes[gi]) ? 2 : 1;
+      lanes_of[size_t(gi)] = s16_ok(scheme, max_bound_bucket[gi]) ? 2 : 1;
       uint64_t h = 1469598103934665603ull;
       for (int32_t id : buckets[size_t(gi)]) h = (h ^ uint64_t(id)) * 1099511628211ull;
       key += "|" + std::to_string(ta::kGridSizes[gi]) + ":" + std::to_string(lanes_of[size_t(gi)]) + ":" +
@@ -586,7 +651,8 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
         size_t used = 0;  // uint4 units
         while (pos < ids.size()) {
           const int32_t id = ids[pos];
-          const size_t need = size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * 4;
+          const Blocks blk = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], g);
+          const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * 4;
           if (!chunk.empty() && (used + need) * 16 > budget) break;
           diroff[size_t(id)] = int64_t(used);
           used += need;

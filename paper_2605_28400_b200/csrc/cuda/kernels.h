@@ -23,54 +23,63 @@ struct KernelEntry {
   int grid = 0;
 };
 
-// lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace requires lanes == 1.
-KernelEntry kernel_g4(int lanes, int mode, bool trace);
-KernelEntry kernel_g8(int lanes, int mode, bool trace);
-KernelEntry kernel_g12(int lanes, int mode, bool trace);
-KernelEntry kernel_g16(int lanes, int mode, bool trace);
+// lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace requires lanes == 1;
+// blocks (multi-block long-triplet support) exists for the largest grid only.
+KernelEntry kernel_g4(int lanes, int mode, bool trace, bool blocks);
+KernelEntry kernel_g8(int lanes, int mode, bool trace, bool blocks);
+KernelEntry kernel_g12(int lanes, int mode, bool trace, bool blocks);
+KernelEntry kernel_g16(int lanes, int mode, bool trace, bool blocks);
 
-inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace) {
+inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, bool blocks) {
   switch (grid) {
-    case 4: return kernel_g4(lanes, mode, trace);
-    case 8: return kernel_g8(lanes, mode, trace);
-    case 12: return kernel_g12(lanes, mode, trace);
-    case 16: return kernel_g16(lanes, mode, trace);
+    case 4: return kernel_g4(lanes, mode, trace, blocks);
+    case 8: return kernel_g8(lanes, mode, trace, blocks);
+    case 12: return kernel_g12(lanes, mode, trace, blocks);
+    case 16: return kernel_g16(lanes, mode, trace, blocks);
   }
   return {};
 }
 
 }  // namespace ta
 
-#define TA_DEFINE_KERNEL_TABLE(G)                                                      \
+#define TA_DEFINE_KERNEL_TABLE(G, WITH_BLOCKS)                                         \
   namespace ta {                                                                       \
-  template <int L, int M, bool TR>                                                     \
+  template <int L, int M, bool TR, bool BL>                                            \
   static KernelEntry entry_##G() {                                                     \
-    return KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR>,                         \
+    return KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR, BL>,                     \
                        WaveSmem<kTileN, G, L>::bytes, G * G, G};                       \
   }                                                                                    \
-  KernelEntry kernel_g##G(int lanes, int mode, bool trace) {                           \
+  template <bool BL>                                                                   \
+  static KernelEntry pick_##G(int lanes, int mode, bool trace) {                       \
     if (trace) {                                                                       \
       if (lanes != 1) return {};                                                       \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<1, kGlobal, true>();                            \
-        case kSemi: return entry_##G<1, kSemi, true>();                                \
-        case kLocal: return entry_##G<1, kLocal, true>();                              \
+        case kGlobal: return entry_##G<1, kGlobal, true, BL>();                        \
+        case kSemi: return entry_##G<1, kSemi, true, BL>();                            \
+        case kLocal: return entry_##G<1, kLocal, true, BL>();                          \
       }                                                                                \
       return {};                                                                       \
     }                                                                                  \
     if (lanes == 1) {                                                                  \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<1, kGlobal, false>();                           \
-        case kSemi: return entry_##G<1, kSemi, false>();                               \
-        case kLocal: return entry_##G<1, kLocal, false>();                             \
+        case kGlobal: return entry_##G<1, kGlobal, false, BL>();                       \
+        case kSemi: return entry_##G<1, kSemi, false, BL>();                           \
+        case kLocal: return entry_##G<1, kLocal, false, BL>();                         \
       }                                                                                \
     } else {                                                                           \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<2, kGlobal, false>();                           \
-        case kSemi: return entry_##G<2, kSemi, false>();                               \
-        case kLocal: return entry_##G<2, kLocal, false>();                             \
+        case kGlobal: return entry_##G<2, kGlobal, false, BL>();                       \
+        case kSemi: return entry_##G<2, kSemi, false, BL>();                           \
+        case kLocal: return entry_##G<2, kLocal, false, BL>();                         \
       }                                                                                \
     }                                                                                  \
     return {};                                                                         \
+  }                                                                                    \
+  KernelEntry kernel_g##G(int lanes, int mode, bool trace, bool blocks) {              \
+    if (blocks) {                                                                      \
+      if constexpr (WITH_BLOCKS) return pick_##G<true>(lanes, mode, trace);            \
+      return {};                                                                       \
+    }                                                                                  \
+    return pick_##G<false>(lanes, mode, trace);                                        \
   }                                                                                    \
   }

@@ -48,7 +48,7 @@ struct TripletDesc {
 struct WaveArgs {
   const uint32_t* __restrict__ seq;        // 2-bit packed, 16 bases per word
   const TripletDesc* __restrict__ desc;
-  const int32_t* __restrict__ items;       // stream item lists (triplet ids)
+  const int4* __restrict__ items;          // stream items {tid, J<<16|K, slices, Bj<<16|Bk}
   const int32_t* __restrict__ stream_off;  // [gridDim.x * LANES + 1]
   const int32_t* __restrict__ cta_steps;   // [gridDim.x]
   int32_t* __restrict__ out_score;
@@ -59,7 +59,20 @@ struct WaveArgs {
   int32_t match_p;                         // sigma' of equal residues   (match - g2)
   int32_t mismatch_p;                      // sigma' of unequal residues (mismatch - g2)
   int32_t g2;                              // 2 * gap (<= 0)
+  uint32_t one;                            // == 1; keeps packed adds on the FMA pipe (IMAD)
+  int32_t* __restrict__ faces;             // block-boundary faces of long triplets (int32 lane values)
+  const int64_t* __restrict__ face_off;    // per stream, in words
 };
+
+// Long triplets are split into row-major G*N x G*N blocks of the (j, k)
+// plane; block (J, K) receives its top face (row J*GN - 1, GN + 1 values
+// incl. the corner) and its left face (column K*GN - 1, GN values) per slice
+// from global memory.  Per stream and triplet the face buffer holds
+//   Fdown  [Bk][a + 1][GN + 1]   written by block (J, K), read by (J + 1, K)
+//   Fright [a + 1][GN]           written by block (J, K), read by (J, K + 1)
+__host__ __device__ inline int64_t face_words(int a, int bk, int gn) {
+  return int64_t(bk) * (a + 1) * (gn + 1) + int64_t(a + 1) * gn;
+}
 
 template <int LANES>
 struct LaneOps;
@@ -108,6 +121,42 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t s) {
   return d;
 }
 
+// d = a * one + c on the FMA pipe (one == 1 at run time): the packed lane add
+// of the t1 partial sum leaves the ALU pipe, which bounds the recurrence.
+__device__ __forceinline__ uint32_t fma_add(uint32_t a, uint32_t one, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(c));
+  return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar, uint32_t count) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared.b64 st, [%0], %1;\n}" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+               "r"(count)
+               : "memory");
+}
+
+// One aggregated arrival per converged group of threads (every thread is
+// counted exactly once, whichever branch it is in).
+__device__ __forceinline__ void mbar_arrive_group(uint64_t* bar) {
+  const uint32_t m = __activemask();
+  __syncwarp(m);
+  if ((threadIdx.x & 31) == static_cast<uint32_t>(__ffs(m) - 1)) mbar_arrive(bar, __popc(m));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t lop_sel(uint32_t a, uint32_t b, uint32_t m) {
   return (a & ~m) | (b & m);  // one LOP3
 }
@@ -128,17 +177,19 @@ struct WaveSmem {
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
   static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
-  static constexpr int kLaneFields = 8;                    // cold per-lane state
+  static constexpr int kLaneFields = 12;                   // cold per-lane state
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
-  static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane;
+  static constexpr size_t kStage = size_t(LANES) * 2 * G * (N + 1) * 4;  // prefetched block faces
+  static constexpr size_t kBar = 16;                       // two mbarriers (mailbox parity)
+  static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane + kStage + kBar;
 };
 
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kBestV, kBestLin };
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kBestV, kBestLin, kOrgJ, kOrgK, kLen, kBk };
 
 // ---------------------------------------------------------------------------
-template <int N, int G, int LANES, int MODE, bool TRACE>
+template <int N, int G, int LANES, int MODE, bool TRACE, bool BLOCKS>
 __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args) {
   static_assert(!TRACE || LANES == 1, "direction cube uses int32 lanes");
   static_assert((N * N) % 4 == 0, "tile cells must group by 4");
@@ -152,6 +203,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   constexpr int SH = TRACE ? 4 : 0;  // value scale 2^SH (tags in low bits)
   constexpr uint32_t NEG = TRACE ? 0xF0000000u : Ops::kNeg;
   constexpr uint32_t kDone = 1u, kOwner = 2u, kBestOk = 4u;
+  constexpr uint32_t kInTop = 8u, kInLeft = 16u, kOutDown = 32u, kOutRight = 64u;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint4* const s12v = reinterpret_cast<uint4*>(smem_raw);                     // [NN/4][T]
@@ -160,6 +212,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   unsigned char* const tab2 = tab1 + SM::kTab;
   uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);        // [2][XW][T+1]
   int32_t* const lst = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX);  // [LANES][8][T]
+  int32_t* const stage = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX + SM::kLane);  // [LANES][2G][N+1]
+  uint64_t* const mbar = reinterpret_cast<uint64_t*>(tab2 + SM::kTab + SM::kX + SM::kLane + SM::kStage);
+  constexpr int GN = G * N;
 
   const int t = threadIdx.x;
   // Thread -> tile map in anti-diagonal order: a warp spans only 2-3
@@ -184,9 +239,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   const int skew = r + cc;
   const int g2 = args.g2;
   const int ag2 = -g2;
+  const uint32_t one = args.one;
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
   for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
+  if (t == 0) {
+    mbar_init(&mbar[0], T);
+    mbar_init(&mbar[1], T);
+  }
 
   // hot per-lane state in registers
   int si[LANES], la[LANES];
@@ -207,13 +267,20 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     return codes;
   };
 
-  // Loads triplet `id` (or the null triplet, id < 0: all-zero weights, which
-  // keeps an idle lane's values bounded) into lane l of this thread: sigma
-  // tables in shared memory, lengths, flags.
-  auto setup = [&](int l, int id) {
-    int a_ = 0x3FFFFFFF, b_ = -1, c_ = -1;
+  // Loads stream item `it` of lane l (or the null item when it >= end: all
+  // zero weights, which keeps an idle lane's values bounded): sigma tables
+  // in shared memory, lengths, block origin, flags.
+  auto setup = [&](int l, int it, int iend) {
+    int id = -1, a_ = 0, b_ = -1, c_ = -1, len = 0x3FFFFFFF, J = 0, K = 0, Bj = 1, Bk = 1;
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
-    if (id >= 0) {
+    if (it < iend) {
+      const int4 rec = __ldg(args.items + it);
+      id = rec.x;
+      J = rec.y >> 16;
+      K = rec.y & 0xFFFF;
+      len = rec.z;
+      Bj = rec.w >> 16;
+      Bk = rec.w & 0xFFFF;
       const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(args.desc + id));
       const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(args.desc + id) + 1);
       a_ = static_cast<int>(d0.x);
@@ -228,13 +295,22 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kLenB) = b_;
     LS(l, kLenC) = c_;
     LS(l, kW0) = static_cast<int32_t>(ww0);
+    LS(l, kOrgJ) = J * GN;
+    LS(l, kOrgK) = K * GN;
+    LS(l, kLen) = len;
+    LS(l, kBk) = Bk;
+    const int gj0 = J * GN + j0, gk0 = K * GN + k0;
     uint32_t f = id >= 0 ? 0u : kDone;
-    if (id >= 0 && b_ / N == r && c_ / N == cc) f |= kOwner;
+    if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
+    if (id >= 0 && J > 0) f |= kInTop;
+    if (id >= 0 && K > 0) f |= kInLeft;
+    if (id >= 0 && J + 1 < Bj) f |= kOutDown;
+    if (id >= 0 && K + 1 < Bk) f |= kOutRight;
     flags[l] = f;
     const int mp = id >= 0 ? args.match_p : 0;
     const int mm = id >= 0 ? args.mismatch_p : 0;
-    const uint32_t c1 = load_codes(ww1, j0 - 1, b_);
-    const uint32_t c2 = load_codes(ww2, k0 - 1, c_);
+    const uint32_t c1 = load_codes(ww1, gj0 - 1, b_);
+    const uint32_t c2 = load_codes(ww2, gk0 - 1, c_);
     if constexpr (LANES == 1) {
       // int16 tables: 4 values (s0 code 0..3) per row, 8 B per (row, thread)
 #pragma unroll
@@ -298,7 +374,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kBestLin) = 0;
     si[l] = 0;
     s0word[l] = 0;
-    setup(l, it < ie ? args.items[it] : -1);
+    setup(l, it, ie);
   }
 
   uint32_t Pv[N + 1][N + 1];
@@ -309,27 +385,64 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
   __syncthreads();
 
+  // Mailbox protocol: step s publishes into xbuf[s & 1] and arrives (one
+  // arrive per warp) on mbar[s & 1]; step s+1 waits for that phase before it
+  // reads.  A thread publishing at step s+1 has waited for every thread's
+  // step-s arrival, which follows that thread's step-s reads of the same
+  // buffer, so the double buffer is race-free without a CTA-wide barrier
+  // and the per-step tail work overlaps the slowest warp.
   const int nsteps = args.cta_steps[blockIdx.x];
   for (int s = 0; s < nsteps; ++s) {
     const int buf = s & 1;
     bool any = false;
 #pragma unroll
     for (int l = 0; l < LANES; ++l) any |= !(flags[l] & kDone);
-    if (s >= skew && any) {
-      // ---- 1. new halos (published by the neighbours at step s-1) --------
+    const bool active = s >= skew && any;
+    // Every thread (active or idle) waits for the previous phase before it
+    // arrives again: no thread can arrive on mbar[b] twice within one phase.
+    if (s > 0) mbar_wait(&mbar[buf ^ 1], static_cast<uint32_t>((s - 1) >> 1) & 1u);
+    if (active) {
+      constexpr int NW = (NN + 7) / 8;
       uint32_t Cu[N + 1][N + 1];
+      uint32_t dirw[TRACE ? NW : 1];
+      // ---- 1. new halos (published by the neighbours at step s-1) --------
       const uint32_t* xin = xbuf + (buf ^ 1) * XW * (T + 1);
 #pragma unroll
       for (int q = 0; q <= N; ++q) Cu[0][q] = xin[(N + q) * (T + 1) + up];
 #pragma unroll
       for (int p = 0; p < N; ++p) Cu[p + 1][0] = xin[p * (T + 1) + left];
+      if (BLOCKS && (r == 0 || cc == 0)) {
+        bool top = false, lft = false;
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          top |= r == 0 && (flags[l] & kInTop) && si[l] <= la[l];
+          lft |= cc == 0 && (flags[l] & kInLeft) && si[l] <= la[l];
+        }
+        if (top || lft) {
+          asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+          for (int l = 0; l < LANES; ++l) {
+            const bool ok = si[l] <= la[l];
+            if (r == 0 && (flags[l] & kInTop) && ok) {
+              const int32_t* st = stage + (l * 2 * G + cc) * (N + 1);
+#pragma unroll
+              for (int q = 0; q <= N; ++q) Cu[0][q] = lop_sel(Cu[0][q], Ops::splat(st[q] << SH), Ops::mask(l));
+            }
+            if (cc == 0 && (flags[l] & kInLeft) && ok) {
+              const int32_t* st = stage + (l * 2 * G + G + r) * (N + 1);
+#pragma unroll
+              for (int p = 0; p < N; ++p) Cu[p + 1][0] = lop_sel(Cu[p + 1][0], Ops::splat(st[p] << SH), Ops::mask(l));
+            }
+          }
+        }
+      }
 
       // ---- 2. per-slice sigma row / column tables -----------------------
       uint32_t sel = 0;  // LANES == 2: PRMT selector; LANES == 1: code
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
         const int pos = si[l] - 1;
-        const uint32_t code = pos >= 0 ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
+        const uint32_t code = (pos >= 0 && (!BLOCKS || pos < la[l])) ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
         if constexpr (LANES == 1) {
           sel = code;
         } else {
@@ -366,25 +479,27 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int l = 0; l < LANES; ++l) {
         const bool live = !(flags[l] & kDone);
         if constexpr (MODE == kGlobal) {
-          if (t == 0 && live && si[l] == 0) fcorner = lop_sel(fcorner, 0u, Ops::mask(l));
+          if (t == 0 && live && si[l] == 0 && LS(l, kOrgJ) == 0 && LS(l, kOrgK) == 0)
+            fcorner = lop_sel(fcorner, 0u, Ops::mask(l));
         } else if constexpr (MODE == kSemi) {
-          if (t == 0 && live) fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
-          if (live && si[l] == 0 && (r == 0 || cc == 0)) {
+          const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
+          if (t == 0 && live && oj == 0 && ok == 0 && si[l] <= la[l])
+            fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
+          if (live && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0))) {
 #pragma unroll
             for (int q = 0; q < N; ++q) {
-              if (r == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (k0 + q)) << SH), Ops::mask(l));
-              if (cc == 0) fcol[q] = lop_sel(fcol[q], Ops::splat((ag2 * (j0 + q)) << SH), Ops::mask(l));
+              if (r == 0 && oj == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (ok + k0 + q)) << SH), Ops::mask(l));
+              if (cc == 0 && ok == 0) fcol[q] = lop_sel(fcol[q], Ops::splat((ag2 * (oj + j0 + q)) << SH), Ops::mask(l));
             }
           }
         } else {
-          // local floor base: |g2| * (i + j0 + k0)
-          flbase = lop_sel(flbase, Ops::splat((ag2 * (si[l] + j0 + k0)) << SH), Ops::mask(l));
+          // local floor base: |g2| * (i + j + k) at the tile origin
+          flbase = lop_sel(flbase, Ops::splat((ag2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0)) << SH),
+                           Ops::mask(l));
         }
       }
 
       // ---- 4. the tile: 6 integer instructions per cell -----------------
-      constexpr int NW = (NN + 7) / 8;
-      uint32_t dirw[TRACE ? NW : 1];
       if constexpr (TRACE) {
 #pragma unroll
         for (int w = 0; w < NW; ++w) dirw[w] = 0;
@@ -404,7 +519,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const uint32_t a2 = s02[Q - 1];
           uint32_t x;
           if constexpr (!TRACE) {
-            const uint32_t y = Pv[P - 1][Q - 1] + a1 + a2;         // t1 partial (IADD3)
+            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2);  // t1 partial (FMA pipe)
             x = Ops::addmax(Pv[P - 1][Q], a1, Pv[P][Q]);             // max(t2, t5)
             x = Ops::addmax(Pv[P][Q - 1], a2, x);                    // t3
             x = Ops::addmax(y, sg, x);                               // t1
@@ -412,7 +527,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::max3(x, Cu[P - 1][Q], Cu[P][Q - 1]);            // t6, t7
           } else {
             // tags: t1 = 5+4+3 = 12 (a1, a2, sg carry 5, 4, 3)
-            const uint32_t y = Pv[P - 1][Q - 1] + a1 + a2;
+            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2);
             x = Ops::addmax(Pv[P - 1][Q], a1, Cu[P][Q - 1]);         // max(t2, t7)
             x = Ops::addmax(Pv[P][Q - 1], a2, x);                    // t3
             x = Ops::addmax(y, sg, x);                               // t1
@@ -442,11 +557,38 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int p = 0; p < N; ++p) xout[p * (T + 1)] = Cu[p + 1][N];
 #pragma unroll
       for (int q = 0; q <= N; ++q) xout[(N + q) * (T + 1)] = Cu[N][q];
+      if (BLOCKS && (r == G - 1 || cc == G - 1)) {
+        bool wrote = false;
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (si[l] > la[l]) continue;
+          const bool dn = r == G - 1 && (flags[l] & kOutDown);
+          const bool rt = cc == G - 1 && (flags[l] & kOutRight);
+          if (!dn && !rt) continue;
+          const int a1 = la[l] + 1;
+          int32_t* fb = args.faces + args.face_off[sbase + l];
+          if (dn) {  // Fdown[K][i][cN + q], q = 0 is the corner (k = cN - 1)
+            int32_t* d = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
+#pragma unroll
+            for (int q = 0; q <= N; ++q) d[q] = Ops::lane(Cu[N][q], l) >> SH;
+          }
+          if (rt) {  // Fright[i][rN + p]
+            int32_t* d = fb + int64_t(LS(l, kBk)) * a1 * (GN + 1) + int64_t(si[l]) * GN + r * N;
+#pragma unroll
+            for (int p = 0; p < N; ++p) d[p] = Ops::lane(Cu[p + 1][N], l) >> SH;
+          }
+          wrote = true;
+        }
+        if (wrote) __threadfence_block();
+      }
+      mbar_arrive_group(&mbar[buf]);
 
       // ---- 6. direction cube slot (64 B per tile-slice) -----------------
       if constexpr (TRACE) {
-        if (!(flags[0] & kDone)) {
-          uint4* dst = args.dirs + args.dir_off[LS(0, kTid)] + (size_t(si[0]) * T + tile) * 4;
+        if (!(flags[0] & kDone) && si[0] <= la[0]) {
+          const int a1 = la[0] + 1;
+          const int blk = (LS(0, kOrgJ) / GN) * LS(0, kBk) + LS(0, kOrgK) / GN;
+          uint4* dst = args.dirs + args.dir_off[LS(0, kTid)] + ((size_t(blk) * a1 + si[0]) * T + tile) * 4;
 #pragma unroll
           for (int v = 0; v < 4; ++v) {
             if (v * 4 < NW) {
@@ -465,7 +607,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         for (int l = 0; l < LANES; ++l) {
           if ((flags[l] & kOwner) && si[l] == la[l]) {
             const int B = LS(l, kLenB), C = LS(l, kLenC), id = LS(l, kTid);
-            const int want = (B - j0 + 1) * (N + 1) + (C - k0 + 1);
+            const int want = (B - LS(l, kOrgJ) - j0 + 1) * (N + 1) + (C - LS(l, kOrgK) - k0 + 1);
             uint32_t v = 0;
 #pragma unroll
             for (int P = 1; P <= N; ++P)
@@ -487,10 +629,10 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         bool anyc = false;
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
-          rb[l] = LS(l, kLenB) - j0;  // rows P-1 <= rb are real
-          cb[l] = LS(l, kLenC) - k0;
+          rb[l] = LS(l, kLenB) - LS(l, kOrgJ) - j0;  // rows P-1 <= rb are real
+          cb[l] = LS(l, kLenC) - LS(l, kOrgK) - k0;
           last[l] = si[l] == la[l];
-          const bool inside = !(flags[l] & kDone) && rb[l] >= 0 && cb[l] >= 0;
+          const bool inside = !(flags[l] & kDone) && si[l] <= la[l] && rb[l] >= 0 && cb[l] >= 0;
           cand[l] = MODE == kLocal ? inside : inside && (last[l] || rb[l] < N || cb[l] < N);
           anyc |= cand[l];
         }
@@ -518,7 +660,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           for (int l = 0; l < LANES; ++l) {
             if (!cand[l]) continue;
             const int sm = Ops::lane(stepmax, l);
-            const int mval = (sm + ((g2 * (si[l] + j0 + k0)) << SH)) >> SH;
+            const int mval = (sm + ((g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0)) << SH)) >> SH;
             if (!(flags[l] & kBestOk) || mval > LS(l, kBestV)) {
               // first cell (row-major = lexicographic) attaining the maximum
               int fp = 0, fq = 0;
@@ -534,7 +676,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
                     fq = Q - 1;
                   }
                 }
-              const uint32_t j = j0 + fp, k = k0 + fq;
+              const uint32_t j = LS(l, kOrgJ) + j0 + fp, k = LS(l, kOrgK) + k0 + fq;
               LS(l, kBestV) = mval;
               LS(l, kBestLin) = static_cast<int32_t>(
                   (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
@@ -556,7 +698,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int l = 0; l < LANES; ++l) {
         if (flags[l] & kDone) continue;
         si[l] += 1;
-        if (si[l] > la[l]) {
+        if (BLOCKS ? si[l] >= LS(l, kLen) : si[l] > la[l]) {
           if constexpr (MODE != kGlobal) {
             if (flags[l] & kBestOk) {
               const unsigned long long key =
@@ -567,7 +709,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           }
           const int it = LS(l, kItem) + 1;
           LS(l, kItem) = it;
-          setup(l, it < LS(l, kIEnd) ? args.items[it] : -1);
+          setup(l, it, LS(l, kIEnd));
           si[l] = 0;
 #pragma unroll
           for (int P = 0; P <= N; ++P)
@@ -575,14 +717,47 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = lop_sel(Pv[P][Q], NEG, Ops::mask(l));
         }
       }
+    } else {
+      mbar_arrive_group(&mbar[buf]);
     }
     // next slice's s0 word (consumed after the barrier: latency hidden)
 #pragma unroll
     for (int l = 0; l < LANES; ++l) {
       const int pos = si[l] - 1;
-      s0word[l] = (!(flags[l] & kDone) && pos >= 0) ? __ldg(args.seq + static_cast<uint32_t>(LS(l, kW0)) + (pos >> 4)) : 0u;
+      s0word[l] = (!(flags[l] & kDone) && pos >= 0 && (!BLOCKS || pos < la[l]))
+                      ? __ldg(args.seq + static_cast<uint32_t>(LS(l, kW0)) + (pos >> 4))
+                      : 0u;
     }
-    __syncthreads();
+    // next slice's block faces -> shared staging (cp.async: no registers held)
+    if (BLOCKS && (r == 0 || cc == 0)) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        if ((flags[l] & kDone) || si[l] > la[l]) continue;
+        const int a1 = la[l] + 1;
+        const int32_t* fb = args.faces + args.face_off[sbase + l];
+        if (r == 0 && (flags[l] & kInTop)) {
+          const int32_t* src = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
+          int32_t* dst = stage + (l * 2 * G + cc) * (N + 1);
+#pragma unroll
+          for (int q = 0; q <= N; ++q)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(dst + q))),
+                         "l"(src + q)
+                         : "memory");
+        }
+        if (cc == 0 && (flags[l] & kInLeft)) {
+          const int32_t* src = fb + int64_t(LS(l, kBk)) * a1 * (GN + 1) + int64_t(si[l]) * GN + r * N;
+          int32_t* dst = stage + (l * 2 * G + G + r) * (N + 1);
+#pragma unroll
+          for (int p = 0; p < N; ++p)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(dst + p))),
+                         "l"(src + p)
+                         : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   }
 }
 

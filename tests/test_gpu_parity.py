@@ -105,8 +105,6 @@ def test_config_samples_vs_reference(gpu_engine, oracle):
             out = ta.align_arrays(seqs, offs[:3 * n + 1], ta.ScoringScheme(*ent["scheme"]),
                                   ta.AlignmentMode(int(mode)))
             for t in range(n):
-                if max(ent["lengths"][t][1:]) >= 160:
-                    continue
                 assert int(out["score"][t]) == recs[t]["score"], (name, mode, t)
                 assert list(out["end"][t]) == recs[t]["end"], (name, mode, t)
         if "rows_global" in ent:
@@ -114,8 +112,6 @@ def test_config_samples_vs_reference(gpu_engine, oracle):
             out = ta.align_arrays(seqs, offs[:3 * k + 1], ta.ScoringScheme(*ent["scheme"]),
                                   ta.AlignmentMode.Global, with_rows=True, cell_budget=1 << 40)
             for t in range(k):
-                if max(ent["lengths"][t][1:]) >= 160:
-                    continue
                 assert list(out["rows"][t]) == ent["rows_global"][t]["rows"], (name, t)
 
 
@@ -165,3 +161,52 @@ def test_empty_and_degenerate(gpu_engine):
             assert int(out["score"][x]) == want["score"], (mode, t)
             assert list(out["end"][x]) == want["end"], (mode, t)
             assert list(out["rows"][x]) == want["rows"], (mode, t)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_c4_mixed_long_vs_reference(gpu_engine, oracle, mode):
+    """Mixed 64-512 bp (config C4): multi-block items through global faces."""
+    ent = load_golden("configs.json.gz")["C4"]
+    seqs, offs = oracle.generate(ent["sample_spec"], ent["rates"][0], ent["rates"][1], ent["seed"])
+    recs = ent["modes"][str(mode)]
+    n = len(recs)
+    out = ta.align_arrays(seqs, offs[:3 * n + 1], ta.ScoringScheme(*ent["scheme"]), ta.AlignmentMode(mode))
+    for t in range(n):
+        assert int(out["status"][t]) == 0, t
+        assert int(out["score"][t]) == recs[t]["score"], (mode, t, ent["lengths"][t])
+        assert list(out["end"][t]) == recs[t]["end"], (mode, t, ent["lengths"][t])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_long_random_rows_vs_oracle(gpu_engine, oracle, mode):
+    """Ragged long triplets (b or c beyond one 160-cell block, a < G), rows too."""
+    rng = np.random.default_rng(99 + mode)
+    trips = []
+    for lens in [(170, 20, 30), (5, 200, 180), (30, 165, 330), (190, 161, 159), (2, 321, 9), (0, 170, 170),
+                 (161, 0, 161), (240, 250, 260)]:
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in lens))
+    for sch in [(1, -1, -2), (3, -2, -1)]:
+        out = run(trips, sch, mode, rows=True)
+        sc = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.align(t, sch, mode, with_rows=True)
+            assert int(out["status"][x]) == 0 and int(sc["status"][x]) == 0
+            assert int(sc["score"][x]) == want["score"] and list(sc["end"][x]) == want["end"], (sch, mode, x)
+            assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (sch, mode, x)
+            assert list(out["begin"][x]) == want["begin"], (sch, mode, x)
+            assert list(out["rows"][x]) == want["rows"], (sch, mode, x)
+
+
+def test_c5_single_long_triplets_vs_reference(gpu_engine, oracle):
+    """Config C5: single 1000 / 1500 / 2000 bp triplets (one stream, 7x7 to 13x13
+    blocks), global score and end vs the reference tiled engine."""
+    cfgs = load_golden("configs.json.gz")
+    for name in ("C5a", "C5b", "C5c"):
+        ent = cfgs[name]
+        seqs, offs = oracle.generate(ent["sample_spec"], ent["rates"][0], ent["rates"][1], ent["seed"])
+        out = ta.align_arrays(seqs, offs, ta.ScoringScheme(*ent["scheme"]), ta.AlignmentMode.Global,
+                              cfg=ta.EngineConfig(cell_budget=1 << 40))
+        want = ent["modes"]["0"][0]
+        assert int(out["status"][0]) == 0, name
+        assert int(out["score"][0]) == want["score"], name
+        assert list(out["end"][0]) == want["end"], name
