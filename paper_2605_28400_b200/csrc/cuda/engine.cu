@@ -18,6 +18,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -241,10 +242,39 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
 // ---------------------------------------------------------------------------
 // per-device context (stream + events), created lazily
 
+template <class T>
+struct PinnedBuf {
+  T* ptr = nullptr;
+  size_t cap = 0;
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  cudaError_t reserve(size_t n) {
+    if (n <= cap && ptr) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n + n / 4, 1024);
+    cudaError_t e = cudaHostAlloc(&ptr, want * sizeof(T), cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+};
+
 struct DeviceCtx {
   int device = -1;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // H2D / D2H of the pipelined path
   int sms = 0;
+  std::mutex mu;                // one pipelined call at a time per device
+  // cached buffers of the pipelined score path (grow-only)
+  PinnedBuf<uint32_t> h_words[2];
+  PinnedBuf<ta::TripletDesc> h_desc;
+  PinnedBuf<int32_t> h_out;     // score, end (3), per triplet
+  DevBuf<uint32_t> d_words;
+  DevBuf<ta::TripletDesc> d_desc;
+  DevBuf<int32_t> d_score, d_end;
+  DevBuf<unsigned long long> d_key;
 };
 
 std::mutex g_ctx_mu;
@@ -266,6 +296,7 @@ int get_ctx(int device, DeviceCtx** out) {
     ctx->device = device;
     TA_CK(cudaSetDevice(device));
     TA_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    TA_CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
     TA_CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
     g_ctx[device] = std::move(ctx);
   }
@@ -317,7 +348,7 @@ int64_t lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c, int grid
   const int g2 = 2 * s.gap;
   const int64_t gn = int64_t(grid) * ta::kTileN;
   const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
-  const int64_t slices = std::max<int64_t>(a + 1, grid + 1);
+  const int64_t slices = std::max<int64_t>(a + 1, grid + 2 + (grid * grid + 31) / 32);
   return int64_t(s.match - g2) * (slices + ej + ek);
 }
 
@@ -392,11 +423,15 @@ inline Blocks blocks_of(int32_t b, int32_t c, int grid) {
   return Blocks{(b + 1 + gn - 1) / gn, (c + 1 + gn - 1) / gn};
 }
 
-// slices one block item occupies in a stream: a+1, padded to >= G+1 for
-// multi-block triplets so a block's faces are written >= 2 steps before the
-// next block's edge tiles prefetch them.
+// slices one block item occupies in a stream: a+1, padded for multi-block
+// triplets so that a block's faces are written well before the next block's
+// edge tiles prefetch them: G+1 steps in lockstep, plus the largest drift
+// between warps under per-warp synchronisation (warps - 1 steps), which is
+// also the length of the mbarrier release/acquire chain that makes the
+// face stores visible to the prefetching warp.
 inline int item_len(int32_t a, const Blocks& bl, int grid) {
-  return (bl.bj * bl.bk > 1) ? std::max(a + 1, grid + 1) : a + 1;
+  const int warps = (grid * grid + 31) / 32;
+  return (bl.bj * bl.bk > 1) ? std::max(a + 1, grid + 2 + warps) : a + 1;
 }
 
 // Greedy least-loaded assignment of triplets to CTA lane streams (the
@@ -705,6 +740,240 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   return TA_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined one-shot score path (ta_align_batch without rows).
+//
+// The batch is cut into contiguous chunks.  For chunk k the host packs ASCII
+// -> 2-bit words with all cores straight into pinned memory, the copy stream
+// moves them (4x fewer bytes than ASCII) while the compute stream still runs
+// chunk k-1, and chunk k's results come back asynchronously: host packing,
+// planning and both copies hide behind the kernels.
+
+struct Lut {
+  uint8_t v[256];
+  Lut() {
+    for (int i = 0; i < 256; ++i) v[i] = 0xFF;
+    v['A'] = 0;
+    v['C'] = 1;
+    v['G'] = 2;
+    v['T'] = 3;
+  }
+};
+
+// Packs the sequences of triplets [lo, hi) (their words are contiguous,
+// starting at global word `wbase`) into dst; flags non-ACGT triplets.
+void host_pack(const char* seqs, const int64_t* offs, int64_t lo, int64_t hi, const std::vector<uint32_t>& wofs,
+               uint32_t wbase, uint32_t* dst, std::vector<int32_t>& status, int threads) {
+  static const Lut lut;
+  auto work = [&](int64_t a0, int64_t a1) {
+    for (int64_t t = a0; t < a1; ++t) {
+      uint8_t orv = 0;
+      for (int d = 0; d < 3; ++d) {
+        const int64_t s0 = offs[3 * t + d], L = offs[3 * t + d + 1] - s0;
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(seqs + s0);
+        uint32_t* out = dst + (wofs[size_t(3 * t + d)] - wbase);
+        const int64_t nw = (L + 15) >> 4;
+        for (int64_t w = 0; w < nw; ++w) {
+          const int64_t base = w * 16, cnt = std::min<int64_t>(16, L - base);
+          uint32_t word = 0;
+          for (int64_t q = 0; q < cnt; ++q) {
+            const uint8_t code = lut.v[src[base + q]];
+            orv |= code;
+            word |= uint32_t(code & 3u) << (2 * q);
+          }
+          out[w] = word;
+        }
+      }
+      if (orv > 3) status[size_t(t)] = TA_ERR_PARSE;
+    }
+  };
+  const int64_t n = hi - lo;
+  const int nt = int(std::max<int64_t>(1, std::min<int64_t>(threads, n / 256)));
+  if (nt == 1) {
+    work(lo, hi);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nt; ++w) pool.emplace_back(work, lo + n * w / nt, lo + n * (w + 1) / nt);
+  for (auto& th : pool) th.join();
+}
+
+int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offsets, int64_t n,
+                           const ta_scheme& scheme, const ta_options& opt, ta_results* out, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  if (int rc = validate_scheme(scheme)) return rc;
+  if (opt.mode < 0 || opt.mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "unknown alignment mode");
+  const int cfg_rc = validate_options(opt);
+  const std::string cfg_msg = cfg_rc ? g_err : std::string();
+  const size_t nn = size_t(n);
+  std::vector<int32_t> a(nn), b(nn), c(nn), status(nn, TA_OK);
+  std::vector<uint32_t> wofs(3 * nn);
+  uint64_t words = 0;
+  for (size_t t = 0; t < nn; ++t) {
+    for (int d = 0; d < 3; ++d) {
+      const int64_t L = offsets[3 * t + d + 1] - offsets[3 * t + d];
+      if (L < 0 || L > (int64_t(1) << 24))
+        return fail(TA_ERR_INVALID_ARGUMENT, "bad sequence offsets for triplet " + std::to_string(t));
+      wofs[3 * t + d] = uint32_t(words);
+      words += uint64_t((L + 15) / 16);
+    }
+    a[t] = int32_t(offsets[3 * t + 1] - offsets[3 * t]);
+    b[t] = int32_t(offsets[3 * t + 2] - offsets[3 * t + 1]);
+    c[t] = int32_t(offsets[3 * t + 3] - offsets[3 * t + 2]);
+  }
+  if (words > 0xFFFFFFF0ull) return fail(TA_ERR_CAPACITY, "batch exceeds 2^32 packed words");
+  // engine errors per triplet, where the reference raises them (tiled.cpp:8-15, 37-58)
+  for (size_t t = 0; t < nn; ++t) {
+    if (cfg_rc) {
+      status[t] = cfg_rc;
+      continue;
+    }
+    if (uint64_t(a[t]) * uint64_t(b[t]) * uint64_t(c[t]) > opt.cell_budget) {
+      status[t] = TA_ERR_CAPACITY;
+      continue;
+    }
+    const int32_t width = opt.team_width > 0 ? opt.team_width : derive_team_width(opt.tile_size, b[t], c[t]);
+    if (int64_t(width) * opt.tile_size < std::max(b[t], c[t])) {
+      status[t] = TA_ERR_CONFIG;
+      continue;
+    }
+    if (opt.mode != TA_GLOBAL && uint64_t(a[t] + 1) * uint64_t(b[t] + 1) * uint64_t(c[t] + 1) > 0xFFFFFFFFull)
+      status[t] = TA_ERR_CAPACITY;  // lexicographic key needs < 2^32 cells
+  }
+  TA_CK(ctx->d_words.reserve(size_t(words) + 2));
+  TA_CK(ctx->d_desc.reserve(nn));
+  TA_CK(ctx->d_score.reserve(nn));
+  TA_CK(ctx->d_end.reserve(3 * nn));
+  TA_CK(ctx->d_key.reserve(nn));
+  TA_CK(ctx->h_desc.reserve(nn));
+  TA_CK(ctx->h_out.reserve(4 * nn));
+  for (size_t t = 0; t < nn; ++t)
+    ctx->h_desc.ptr[t] = ta::TripletDesc{a[t], b[t], c[t], 0, wofs[3 * t], wofs[3 * t + 1], wofs[3 * t + 2], 0};
+  // chunks: contiguous triplet ranges of ~equal cells
+  int64_t total_cells = 0;
+  for (size_t t = 0; t < nn; ++t) total_cells += int64_t(a[t]) * b[t] * c[t];
+  const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(16, n / 20000));
+  std::vector<int64_t> cut{0};
+  {
+    int64_t acc = 0, k = 1;
+    for (int64_t t = 0; t < n; ++t) {
+      acc += int64_t(a[size_t(t)]) * b[size_t(t)] * c[size_t(t)];
+      if (k < nchunks && acc * nchunks >= total_cells * k && t + 1 < n) {
+        cut.push_back(t + 1);
+        ++k;
+      }
+    }
+    cut.push_back(n);
+  }
+  const int threads = int(std::max(1u, std::thread::hardware_concurrency()));
+  const int g2 = 2 * scheme.gap;
+  ta::WaveArgs base{};
+  base.seq = ctx->d_words.ptr;
+  base.desc = ctx->d_desc.ptr;
+  base.out_score = ctx->d_score.ptr;
+  base.out_end = ctx->d_end.ptr;
+  base.out_key = ctx->d_key.ptr;
+  base.g2 = g2;
+  base.match_p = scheme.match - g2;
+  base.mismatch_p = scheme.mismatch - g2;
+  base.one = 1u;
+  cudaEvent_t slot_free[2], h2d_done, kdone;
+  for (auto& e : slot_free) TA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  TA_CK(cudaEventCreateWithFlags(&h2d_done, cudaEventDisableTiming));
+  TA_CK(cudaEventCreateWithFlags(&kdone, cudaEventDisableTiming));
+  TA_CK(cudaMemcpyAsync(ctx->d_desc.ptr, ctx->h_desc.ptr, nn * sizeof(ta::TripletDesc), cudaMemcpyHostToDevice,
+                        ctx->copy));
+  // the batch shim lends lengths and the SM count to plan_streams / prepare_bucket
+  ta_batch shim;
+  shim.ctx = ctx;
+  shim.a.swap(a);
+  shim.b.swap(b);
+  shim.c.swap(c);
+  std::vector<std::unique_ptr<BucketLaunch>> keep;  // plans stay alive until the end (no cudaFree mid-pipeline)
+  int64_t launches = 0;
+  int rc = TA_OK;
+  for (size_t k = 0; k + 1 < cut.size() && rc == TA_OK; ++k) {
+    const int64_t lo = cut[k], hi = cut[k + 1];
+    if (hi <= lo) continue;
+    const uint32_t w0 = wofs[3 * size_t(lo)];
+    const uint32_t w1 = hi < n ? wofs[3 * size_t(hi)] : uint32_t(words);
+    PinnedBuf<uint32_t>& slot = ctx->h_words[k & 1];
+    TA_CK(cudaEventSynchronize(slot_free[k & 1]));  // the previous H2D from this slot is done
+    TA_CK(slot.reserve(size_t(w1 - w0) + 2));
+    host_pack(seqs, offsets, lo, hi, wofs, w0, slot.ptr, status, threads);
+    TA_CK(cudaMemcpyAsync(ctx->d_words.ptr + w0, slot.ptr, size_t(w1 - w0) * 4, cudaMemcpyHostToDevice, ctx->copy));
+    TA_CK(cudaEventRecord(slot_free[k & 1], ctx->copy));
+    std::vector<std::vector<int32_t>> buckets(ta::kNumGrid);
+    int64_t max_bound[ta::kNumGrid] = {0};
+    std::vector<int32_t> ok_ids;
+    for (int64_t t = lo; t < hi; ++t) {
+      if (status[size_t(t)] != TA_OK) continue;
+      const int32_t A = shim.a[size_t(t)], B = shim.b[size_t(t)], C = shim.c[size_t(t)];
+      const int g = pick_grid(B, C);
+      int gi = 0;
+      while (ta::kGridSizes[gi] != g) ++gi;
+      buckets[size_t(gi)].push_back(int32_t(t));
+      max_bound[gi] = std::max(max_bound[gi], lane_bound(scheme, A, B, C, g));
+      ok_ids.push_back(int32_t(t));
+    }
+    std::vector<BucketLaunch*> launch_now;
+    for (int gi = 0; gi < ta::kNumGrid && rc == TA_OK; ++gi) {
+      if (buckets[size_t(gi)].empty()) continue;
+      keep.push_back(std::make_unique<BucketLaunch>());
+      const int lanes = s16_ok(scheme, max_bound[gi]) ? 2 : 1;
+      rc = prepare_bucket(&shim, buckets[size_t(gi)], ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy,
+                          keep.back().get());
+      launch_now.push_back(keep.back().get());
+    }
+    if (rc != TA_OK) break;
+    DevBuf<int32_t>* ids_buf = nullptr;
+    if (opt.mode != TA_GLOBAL && !ok_ids.empty()) {
+      keep.push_back(std::make_unique<BucketLaunch>());
+      ids_buf = &keep.back()->soff;
+      TA_CK(ids_buf->reserve(ok_ids.size()));
+      TA_CK(cudaMemcpyAsync(ids_buf->ptr, ok_ids.data(), ok_ids.size() * 4, cudaMemcpyHostToDevice, ctx->copy));
+      TA_CK(cudaMemsetAsync(ctx->d_key.ptr + lo, 0, size_t(hi - lo) * 8, ctx->copy));
+    }
+    TA_CK(cudaEventRecord(h2d_done, ctx->copy));
+    TA_CK(cudaStreamWaitEvent(st, h2d_done, 0));
+    for (BucketLaunch* bl : launch_now) {
+      rc = launch_prepared(bl, base, st, &launches);
+      if (rc != TA_OK) break;
+    }
+    if (rc != TA_OK) break;
+    if (ids_buf) {
+      const int64_t m = int64_t(ok_ids.size());
+      decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(ctx->d_key.ptr, ctx->d_desc.ptr, ids_buf->ptr, m,
+                                                                  ctx->d_score.ptr, ctx->d_end.ptr);
+      TA_CK(cudaGetLastError());
+    }
+    TA_CK(cudaEventRecord(kdone, st));
+    TA_CK(cudaStreamWaitEvent(ctx->copy, kdone, 0));
+    TA_CK(cudaMemcpyAsync(ctx->h_out.ptr + lo, ctx->d_score.ptr + lo, size_t(hi - lo) * 4, cudaMemcpyDeviceToHost,
+                          ctx->copy));
+    TA_CK(cudaMemcpyAsync(ctx->h_out.ptr + nn + 3 * size_t(lo), ctx->d_end.ptr + 3 * lo, size_t(hi - lo) * 12,
+                          cudaMemcpyDeviceToHost, ctx->copy));
+  }
+  const cudaError_t e1 = cudaStreamSynchronize(ctx->copy);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  for (auto& e : slot_free) cudaEventDestroy(e);
+  cudaEventDestroy(h2d_done);
+  cudaEventDestroy(kdone);
+  if (rc != TA_OK) return rc;
+  TA_CK(e1);
+  TA_CK(e2);
+  for (size_t t = 0; t < nn; ++t) {
+    const bool ok = status[t] == TA_OK;
+    if (out->scores) out->scores[t] = ok ? ctx->h_out.ptr[t] : 0;
+    if (out->ends)
+      for (int d = 0; d < 3; ++d) out->ends[3 * t + d] = ok ? ctx->h_out.ptr[nn + 3 * t + d] : 0;
+    if (out->status) out->status[t] = status[t];
+  }
+  if (cfg_rc) g_err = cfg_msg;
+  return TA_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -851,6 +1120,13 @@ void ta_batch_destroy(ta_batch* b) {
 int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t n,
                    const ta_scheme* scheme, const ta_options* opt, ta_results* out, void* stream) {
   if (!scheme || !opt || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
+  if (!opt->with_rows && n > 0) {
+    DeviceCtx* ctx = nullptr;
+    if (int rc = get_ctx(device, &ctx)) return rc;
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    return align_scores_pipelined(ctx, seqs, offsets, n, *scheme, *opt, out, st);
+  }
   ta_batch* bt = nullptr;
   if (int rc = ta_batch_create(device, seqs, offsets, n, &bt, stream)) return rc;
   std::unique_ptr<ta_batch, void (*)(ta_batch*)> guard(bt, ta_batch_destroy);

@@ -232,6 +232,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     cc = d - r;
   }
   const int tile = r * G + cc;
+
   const int j0 = r * N;
   const int k0 = cc * N;
   const int left = cc ? tile - 1 : T;
@@ -385,12 +386,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
   __syncthreads();
 
-  // Mailbox protocol: step s publishes into xbuf[s & 1] and arrives (one
-  // arrive per warp) on mbar[s & 1]; step s+1 waits for that phase before it
-  // reads.  A thread publishing at step s+1 has waited for every thread's
-  // step-s arrival, which follows that thread's step-s reads of the same
-  // buffer, so the double buffer is race-free without a CTA-wide barrier
-  // and the per-step tail work overlaps the slowest warp.
+  // Mailbox protocol: step s publishes into xbuf[s & 1] and arrives on
+  // mbar[s & 1]; step s+1 waits for that phase before it reads.  A thread
+  // publishing at step s+1 has waited for every thread's step-s arrival,
+  // which follows that thread's step-s reads of the same buffer, so the
+  // double buffer is race-free without __syncthreads and the per-step tail
+  // work (extraction, lane switches, prefetch) overlaps the slowest warp.
   const int nsteps = args.cta_steps[blockIdx.x];
   for (int s = 0; s < nsteps; ++s) {
     const int buf = s & 1;
