@@ -18,6 +18,7 @@
 #include <mutex>
 #include <queue>
 #include <string>
+#include <tuple>
 #include <thread>
 #include <utility>
 #include <vector>
@@ -443,21 +444,61 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
   const int S = ctas * lanes;
   const int gn = grid * ta::kTileN;
   std::vector<std::vector<int32_t>> lists(static_cast<size_t>(S));
-  using Load = std::pair<int64_t, int32_t>;
-  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
-  for (int s = 0; s < S; ++s) heap.push({0, s});
   std::vector<int64_t> load(static_cast<size_t>(S), 0), face(static_cast<size_t>(S), 0);
-  for (int32_t id : ids) {
+  using Load = std::pair<int64_t, int32_t>;
+  auto cost = [&](int32_t id) {
     const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
-    const int64_t len = item_len(a[size_t(id)], bl, grid);
-    Load top = heap.top();
-    heap.pop();
-    lists[size_t(top.second)].push_back(id);
-    top.first += len * bl.bj * bl.bk;
-    load[size_t(top.second)] = top.first;
+    return int64_t(item_len(a[size_t(id)], bl, grid)) * bl.bj * bl.bk;
+  };
+  auto put = [&](int s, int32_t id) {
+    lists[size_t(s)].push_back(id);
+    load[size_t(s)] += cost(id);
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
     if (bl.bj * bl.bk > 1)
-      face[size_t(top.second)] = std::max(face[size_t(top.second)], ta::face_words(a[size_t(id)], bl.bk, gn));
-    heap.push(top);
+      face[size_t(s)] = std::max(face[size_t(s)], ta::face_words(a[size_t(id)], bl.bk, gn));
+  };
+  std::vector<int32_t> singles;
+  if (lanes == 2) {
+    // Pair triplets with identical stream items (slices, Bj, Bk) into the two
+    // lanes of one CTA so both lanes switch triplets in the same step (one
+    // combined table build instead of two divergent ones).  Pairs first,
+    // unpaired triplets at the stream tails.
+    std::vector<int32_t> order(ids);
+    auto key = [&](int32_t id) {
+      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+      return std::make_tuple(item_len(a[size_t(id)], bl, grid), bl.bj, bl.bk);
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int cta = 0; cta < ctas; ++cta) heap.push({0, cta});
+    size_t i = 0;
+    while (i < order.size()) {
+      if (i + 1 < order.size() && key(order[i]) == key(order[i + 1])) {
+        Load top = heap.top();
+        heap.pop();
+        put(top.second * 2, order[i]);
+        put(top.second * 2 + 1, order[i + 1]);
+        top.first += cost(order[i]);
+        heap.push(top);
+        i += 2;
+      } else {
+        singles.push_back(order[i]);
+        i += 1;
+      }
+    }
+  } else {
+    singles = ids;
+  }
+  {
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int s = 0; s < S; ++s) heap.push({load[size_t(s)], s});
+    for (int32_t id : singles) {
+      Load top = heap.top();
+      heap.pop();
+      put(top.second, id);
+      top.first = load[size_t(top.second)];
+      heap.push(top);
+    }
   }
   out->items.clear();
   out->soff.assign(size_t(S) + 1, 0);

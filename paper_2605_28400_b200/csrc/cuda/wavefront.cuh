@@ -268,10 +268,15 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     return codes;
   };
 
+  struct LaneLoad {
+    uint32_t c1, c2;  // 2-bit codes of the tile's N s1 / s2 characters
+    int mp, mm;       // sigma' of equal / unequal residues (0, 0 for the null item)
+  };
+
   // Loads stream item `it` of lane l (or the null item when it >= end: all
-  // zero weights, which keeps an idle lane's values bounded): sigma tables
-  // in shared memory, lengths, block origin, flags.
-  auto setup = [&](int l, int it, int iend) {
+  // zero weights, which keeps an idle lane's values bounded): lengths, block
+  // origin and flags; returns the tile's characters for the sigma tables.
+  auto fetch = [&](int l, int it, int iend) -> LaneLoad {
     int id = -1, a_ = 0, b_ = -1, c_ = -1, len = 0x3FFFFFFF, J = 0, K = 0, Bj = 1, Bk = 1;
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
     if (it < iend) {
@@ -308,10 +313,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     if (id >= 0 && J + 1 < Bj) f |= kOutDown;
     if (id >= 0 && K + 1 < Bk) f |= kOutRight;
     flags[l] = f;
-    const int mp = id >= 0 ? args.match_p : 0;
-    const int mm = id >= 0 ? args.mismatch_p : 0;
-    const uint32_t c1 = load_codes(ww1, gj0 - 1, b_);
-    const uint32_t c2 = load_codes(ww2, gk0 - 1, c_);
+    return LaneLoad{load_codes(ww1, gj0 - 1, b_), load_codes(ww2, gk0 - 1, c_), id >= 0 ? args.match_p : 0,
+                    id >= 0 ? args.mismatch_p : 0};
+  };
+
+  // sigma tables of one lane (the other lane's halves are left untouched)
+  auto tables_lane = [&](int l, const LaneLoad& ld) {
+    const uint32_t c1 = ld.c1, c2 = ld.c2;
+    const int mp = ld.mp, mm = ld.mm;
     if constexpr (LANES == 1) {
       // int16 tables: 4 values (s0 code 0..3) per row, 8 B per (row, thread)
 #pragma unroll
@@ -364,7 +373,43 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     }
   };
 
+  // sigma tables of both s16x2 lanes at once (paired lane switch): one PRMT
+  // per cell builds the packed word, written 4 cells per STS.128.
+  auto tables_both = [&](const LaneLoad& l0, const LaneLoad& l1) {
+    const uint32_t m0 = static_cast<uint32_t>(l0.mm) * 0x01010101u, d0 = static_cast<uint32_t>(l0.mp - l0.mm);
+    const uint32_t m1 = static_cast<uint32_t>(l1.mm) * 0x01010101u, d1 = static_cast<uint32_t>(l1.mp - l1.mm);
+    uint32_t t2a[N], t2b[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      const uint32_t x10 = (l0.c1 >> (2 * p)) & 3u, x20 = (l0.c2 >> (2 * p)) & 3u;
+      const uint32_t x11 = (l1.c1 >> (2 * p)) & 3u, x21 = (l1.c2 >> (2 * p)) & 3u;
+      reinterpret_cast<uint2*>(tab1)[p * T + t] = make_uint2(m0 + (d0 << (8 * x10)), m1 + (d1 << (8 * x11)));
+      t2a[p] = m0 + (d0 << (8 * x20));
+      t2b[p] = m1 + (d1 << (8 * x21));
+      reinterpret_cast<uint2*>(tab2)[p * T + t] = make_uint2(t2a[p], t2b[p]);
+    }
+    uint32_t sel[N];
+#pragma unroll
+    for (int p = 0; p < N; ++p) {
+      const uint32_t x10 = (l0.c1 >> (2 * p)) & 3u, x11 = ((l1.c1 >> (2 * p)) & 3u) + 4u;
+      sel[p] = x10 | ((x10 | 8u) << 4) | (x11 << 8) | ((x11 | 8u) << 12);
+    }
+#pragma unroll
+    for (int g = 0; g < NN / 4; ++g) {
+      uint32_t v[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int cell = g * 4 + e, p = cell / N, q = cell % N;
+        v[e] = prmt(t2a[q], t2b[q], sel[p]);
+      }
+      s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+  };
+
+  auto setup = [&](int l, int it, int iend) { tables_lane(l, fetch(l, it, iend)); };
+
   const int sbase = blockIdx.x * LANES;
+  LaneLoad first[LANES];
 #pragma unroll
   for (int l = 0; l < LANES; ++l) {
     const int it = args.stream_off[sbase + l];
@@ -375,7 +420,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kBestLin) = 0;
     si[l] = 0;
     s0word[l] = 0;
-    setup(l, it, ie);
+    first[l] = fetch(l, it, ie);
+  }
+  if constexpr (LANES == 2) {
+    tables_both(first[0], first[1]);
+  } else {
+    tables_lane(0, first[0]);
   }
 
   uint32_t Pv[N + 1][N + 1];
@@ -695,11 +745,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = Cu[P][Q];
 
       // ---- 9. advance the lanes (switch triplets at the end of a stream item)
+      bool sw[LANES];
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
+        sw[l] = false;
         if (flags[l] & kDone) continue;
         si[l] += 1;
-        if (BLOCKS ? si[l] >= LS(l, kLen) : si[l] > la[l]) {
+        sw[l] = BLOCKS ? si[l] >= LS(l, kLen) : si[l] > la[l];
+        if (sw[l]) {
           if constexpr (MODE != kGlobal) {
             if (flags[l] & kBestOk) {
               const unsigned long long key =
@@ -708,6 +761,26 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               atomicMax(args.out_key + LS(l, kTid), key);
             }
           }
+        }
+      }
+      if (LANES == 2 && sw[0] && sw[LANES - 1]) {
+        // paired switch (the host aligns equal-length items in both lanes)
+        const int it0 = LS(0, kItem) + 1, it1 = LS(LANES - 1, kItem) + 1;
+        LS(0, kItem) = it0;
+        LS(LANES - 1, kItem) = it1;
+        const LaneLoad l0 = fetch(0, it0, LS(0, kIEnd));
+        const LaneLoad l1 = fetch(LANES - 1, it1, LS(LANES - 1, kIEnd));
+        if constexpr (LANES == 2) tables_both(l0, l1);
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) si[l] = 0;
+#pragma unroll
+        for (int P = 0; P <= N; ++P)
+#pragma unroll
+          for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = NEG;
+      } else {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          if (!sw[l]) continue;
           const int it = LS(l, kItem) + 1;
           LS(l, kItem) = it;
           setup(l, it, LS(l, kIEnd));
