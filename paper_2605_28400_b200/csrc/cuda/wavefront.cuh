@@ -26,7 +26,9 @@
 //    from a proven bound, so results are bit-identical to the reference.
 #pragma once
 
+#include <climits>
 #include <cstdint>
+#include <type_traits>
 
 namespace ta {
 
@@ -181,12 +183,14 @@ struct WaveSmem {
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
   static constexpr size_t kStage = size_t(LANES) * 2 * G * (N + 1) * 4;  // prefetched block faces
   static constexpr size_t kBar = 16;                       // two mbarriers (mailbox parity)
-  static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane + kStage + kBar;
+  static constexpr int kSlots = 64;                        // open stream items per lane (ring)
+  static constexpr size_t kBest = size_t(LANES) * kSlots * 12;  // per-item best key + finish count
+  static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane + kStage + kBar + kBest;
 };
 
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kBestV, kBestLin, kOrgJ, kOrgK, kLen, kBk };
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kUnused6, kUnused7, kOrgJ, kOrgK, kLen, kBk };
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, bool BLOCKS>
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   constexpr int XW = SM::XW;
   constexpr int SH = TRACE ? 4 : 0;  // value scale 2^SH (tags in low bits)
   constexpr uint32_t NEG = TRACE ? 0xF0000000u : Ops::kNeg;
-  constexpr uint32_t kDone = 1u, kOwner = 2u, kBestOk = 4u;
+  constexpr uint32_t kDone = 1u, kOwner = 2u;
   constexpr uint32_t kInTop = 8u, kInLeft = 16u, kOutDown = 32u, kOutRight = 64u;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -214,6 +218,11 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   int32_t* const lst = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX);  // [LANES][8][T]
   int32_t* const stage = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX + SM::kLane);  // [LANES][2G][N+1]
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(tab2 + SM::kTab + SM::kX + SM::kLane + SM::kStage);
+  // Best (value, cell) of every open stream item, shared by the CTA's threads:
+  // key = (value ^ 2^31) << 32 | ~lin (larger value, then smaller (i, j, k));
+  // bcnt counts threads that finished the item (the last one flushes).
+  unsigned long long* const bkey = reinterpret_cast<unsigned long long*>(mbar + 2);     // [LANES][kSlots]
+  uint32_t* const bcnt = reinterpret_cast<uint32_t*>(bkey + LANES * SM::kSlots);         // [LANES][kSlots]
   constexpr int GN = G * N;
 
   const int t = threadIdx.x;
@@ -244,6 +253,10 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
   for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
+  for (int w = t; w < LANES * SM::kSlots; w += T) {
+    bkey[w] = 0ull;
+    bcnt[w] = 0u;
+  }
   if (t == 0) {
     mbar_init(&mbar[0], T);
     mbar_init(&mbar[1], T);
@@ -270,7 +283,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
   struct LaneLoad {
     uint32_t c1, c2;  // 2-bit codes of the tile's N s1 / s2 characters
+    uint32_t v1, v2;  // bit p: position p holds a real s1 / s2 residue (else padding: sigma' = 0)
     int mp, mm;       // sigma' of equal / unequal residues (0, 0 for the null item)
+  };
+  // positions p in [0, N) with 0 <= g - 1 + p < len
+  auto valid_bits = [](int g, int len) -> uint32_t {
+    const int lo = g == 0 ? 1 : 0;
+    const int hi = max(0, min(N, len - g + 1));
+    return hi > lo ? ((1u << hi) - 1u) & ~((1u << lo) - 1u) : 0u;
   };
 
   // Loads stream item `it` of lane l (or the null item when it >= end: all
@@ -313,8 +333,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     if (id >= 0 && J + 1 < Bj) f |= kOutDown;
     if (id >= 0 && K + 1 < Bk) f |= kOutRight;
     flags[l] = f;
-    return LaneLoad{load_codes(ww1, gj0 - 1, b_), load_codes(ww2, gk0 - 1, c_), id >= 0 ? args.match_p : 0,
-                    id >= 0 ? args.mismatch_p : 0};
+    return LaneLoad{load_codes(ww1, gj0 - 1, b_), load_codes(ww2, gk0 - 1, c_), valid_bits(gj0, b_),
+                    valid_bits(gk0, c_), id >= 0 ? args.match_p : 0, id >= 0 ? args.mismatch_p : 0};
   };
 
   // sigma tables of one lane (the other lane's halves are left untouched)
@@ -329,8 +349,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         uint32_t v1[4], v2[4];
 #pragma unroll
         for (int code = 0; code < 4; ++code) {
-          v1[code] = static_cast<uint32_t>(code == int(x1) ? mp : mm) & 0xFFFFu;
-          v2[code] = static_cast<uint32_t>(code == int(x2) ? mp : mm) & 0xFFFFu;
+          v1[code] = ((ld.v1 >> p) & 1u) ? static_cast<uint32_t>(code == int(x1) ? mp : mm) & 0xFFFFu : 0u;
+          v2[code] = ((ld.v2 >> p) & 1u) ? static_cast<uint32_t>(code == int(x2) ? mp : mm) & 0xFFFFu : 0u;
         }
         reinterpret_cast<uint2*>(tab1)[p * T + t] = make_uint2(v1[0] | (v1[1] << 16), v1[2] | (v1[3] << 16));
         reinterpret_cast<uint2*>(tab2)[p * T + t] = make_uint2(v2[0] | (v2[1] << 16), v2[2] | (v2[3] << 16));
@@ -343,7 +363,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int cell = g * 4 + e, p = cell / N, q = cell % N;
-          v[e] = static_cast<uint32_t>((((c1 >> (2 * p)) & 3u) == ((c2 >> (2 * q)) & 3u) ? mp : mm) * sc + tg);
+          const int sv = ((ld.v1 >> p) & (ld.v2 >> q) & 1u) ? ((((c1 >> (2 * p)) & 3u) == ((c2 >> (2 * q)) & 3u)) ? mp : mm) : 0;
+          v[e] = static_cast<uint32_t>(sv * sc + tg);
         }
         s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
       }
@@ -355,8 +376,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
       for (int p = 0; p < N; ++p) {
         const uint32_t x1 = (c1 >> (2 * p)) & 3u, x2 = (c2 >> (2 * p)) & 3u;
-        reinterpret_cast<uint32_t*>(tab1)[(p * T + t) * 2 + l] = mm8 + (dm << (8 * x1));
-        t2w[p] = mm8 + (dm << (8 * x2));
+        reinterpret_cast<uint32_t*>(tab1)[(p * T + t) * 2 + l] = ((ld.v1 >> p) & 1u) ? mm8 + (dm << (8 * x1)) : 0u;
+        t2w[p] = ((ld.v2 >> p) & 1u) ? mm8 + (dm << (8 * x2)) : 0u;
         reinterpret_cast<uint32_t*>(tab2)[(p * T + t) * 2 + l] = t2w[p];
       }
       uint16_t* s12h = reinterpret_cast<uint16_t*>(s12w);
@@ -367,7 +388,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
         for (int q = 0; q < N; ++q) {
           const int cell = p * N + q;
-          s12h[((size_t(cell >> 2) * T + t) * 4 + (cell & 3)) * 2 + l] = static_cast<uint16_t>(prmt(t2w[q], 0u, sel));
+          s12h[((size_t(cell >> 2) * T + t) * 4 + (cell & 3)) * 2 + l] =
+              ((ld.v1 >> p) & 1u) ? static_cast<uint16_t>(prmt(t2w[q], 0u, sel)) : uint16_t(0);
         }
       }
     }
@@ -383,16 +405,18 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     for (int p = 0; p < N; ++p) {
       const uint32_t x10 = (l0.c1 >> (2 * p)) & 3u, x20 = (l0.c2 >> (2 * p)) & 3u;
       const uint32_t x11 = (l1.c1 >> (2 * p)) & 3u, x21 = (l1.c2 >> (2 * p)) & 3u;
-      reinterpret_cast<uint2*>(tab1)[p * T + t] = make_uint2(m0 + (d0 << (8 * x10)), m1 + (d1 << (8 * x11)));
-      t2a[p] = m0 + (d0 << (8 * x20));
-      t2b[p] = m1 + (d1 << (8 * x21));
+      reinterpret_cast<uint2*>(tab1)[p * T + t] =
+          make_uint2(((l0.v1 >> p) & 1u) ? m0 + (d0 << (8 * x10)) : 0u, ((l1.v1 >> p) & 1u) ? m1 + (d1 << (8 * x11)) : 0u);
+      t2a[p] = ((l0.v2 >> p) & 1u) ? m0 + (d0 << (8 * x20)) : 0u;
+      t2b[p] = ((l1.v2 >> p) & 1u) ? m1 + (d1 << (8 * x21)) : 0u;
       reinterpret_cast<uint2*>(tab2)[p * T + t] = make_uint2(t2a[p], t2b[p]);
     }
-    uint32_t sel[N];
+    uint32_t sel[N], pm[N];
 #pragma unroll
     for (int p = 0; p < N; ++p) {
       const uint32_t x10 = (l0.c1 >> (2 * p)) & 3u, x11 = ((l1.c1 >> (2 * p)) & 3u) + 4u;
       sel[p] = x10 | ((x10 | 8u) << 4) | (x11 << 8) | ((x11 | 8u) << 12);
+      pm[p] = (((l0.v1 >> p) & 1u) ? 0x0000FFFFu : 0u) | (((l1.v1 >> p) & 1u) ? 0xFFFF0000u : 0u);
     }
 #pragma unroll
     for (int g = 0; g < NN / 4; ++g) {
@@ -400,7 +424,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int cell = g * 4 + e, p = cell / N, q = cell % N;
-        v[e] = prmt(t2a[q], t2b[q], sel[p]);
+        v[e] = prmt(t2a[q], t2b[q], sel[p]) & pm[p];
       }
       s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
     }
@@ -416,8 +440,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     const int ie = args.stream_off[sbase + l + 1];
     LS(l, kItem) = it;
     LS(l, kIEnd) = ie;
-    LS(l, kBestV) = 0;
-    LS(l, kBestLin) = 0;
     si[l] = 0;
     s0word[l] = 0;
     first[l] = fetch(l, it, ie);
@@ -522,7 +544,15 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       uint32_t fcorner = NEG;
       uint32_t frow[MODE == kSemi ? N : 1], fcol[MODE == kSemi ? N : 1];
       uint32_t flbase = 0;
+      bool force = false;  // semi: this step computes slice-0 axis cells of a lane
       if constexpr (MODE == kSemi) {
+#pragma unroll
+        for (int l = 0; l < LANES; ++l) {
+          const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
+          force |= !(flags[l] & kDone) && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0));
+        }
+      }
+      if (force) {
 #pragma unroll
         for (int q = 0; q < N; ++q) frow[q] = fcol[q] = NEG;
       }
@@ -536,7 +566,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
           if (t == 0 && live && oj == 0 && ok == 0 && si[l] <= la[l])
             fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
-          if (live && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0))) {
+          if (force && live && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0))) {
 #pragma unroll
             for (int q = 0; q < N; ++q) {
               if (r == 0 && oj == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (ok + k0 + q)) << SH), Ops::mask(l));
@@ -555,13 +585,23 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
         for (int w = 0; w < NW; ++w) dirw[w] = 0;
       }
+      // local floor |g2| * (i + j + k) of the current cell, stepped along the
+      // row on the FMA pipe (values >= 0: packed adds never carry)
+      const uint32_t ag2s = Ops::splat(ag2 * (1 << SH));
+      uint32_t flrow = flbase + (TRACE ? kTagStop : 0u);
+      // The slice-0 axis cells of semi-global mode are forced in a separate
+      // instance of the tile loop, so ordinary steps carry no forcing maxima.
+      auto sweep_tile = [&](auto force_tag) {
+      constexpr bool FORCE = decltype(force_tag)::value;
       uint4 sg4 = make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int P = 1; P <= N; ++P) {
         uint32_t a1 = sig_row(tab1, P - 1);
         if constexpr (TRACE) a1 = a1 * 16u + kTagT2;
-        uint32_t flrow = 0;
-        if constexpr (MODE == kLocal) flrow = flbase + Ops::splat((ag2 * (P - 1)) << SH) + (TRACE ? kTagStop : 0u);
+        uint32_t fl = flrow;
+        if constexpr (MODE == kLocal) {
+          if (P < N) flrow = fma_add(flrow, one, ag2s);
+        }
 #pragma unroll
         for (int Q = 1; Q <= N; ++Q) {
           const int cell = (P - 1) * N + (Q - 1);
@@ -586,11 +626,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::addmax(Pv[P][Q], kTagT5, x);                    // t5
             x = Ops::addmax(Cu[P - 1][Q], kTagT6, x);                // t6
           }
-          if constexpr (MODE == kLocal) x = Ops::addmax(flrow, Ops::splat((ag2 * (Q - 1)) << SH), x);  // floor 0
+          if constexpr (MODE == kLocal) {
+            x = Ops::max2(x, fl);  // floor 0 (oracle.cpp:59)
+            if (Q < N) fl = fma_add(fl, one, ag2s);
+          }
           if constexpr (MODE == kGlobal || MODE == kSemi) {
             if (P == 1 && Q == 1) x = Ops::max2(x, fcorner);
           }
-          if constexpr (MODE == kSemi) {
+          if constexpr (MODE == kSemi && FORCE) {
             if (P == 1) x = Ops::max2(x, frow[Q - 1]);
             if (Q == 1) x = Ops::max2(x, fcol[P - 1]);
           }
@@ -600,6 +643,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           }
           Cu[P][Q] = x;
         }
+      }
+      };
+      if (MODE == kSemi && force) {
+        sweep_tile(std::true_type{});
+      } else {
+        sweep_tile(std::false_type{});
       }
 
       // ---- 5. publish right column / down row (+ corner) ----------------
@@ -675,64 +724,135 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         // Best tracking (oracle.cpp:67-88, tiled.hpp:129-144, 222-228): max
         // value, ties to the lexicographically smallest (i, j, k).
         // Candidates: local = every real cell; semi = i == a || j == b || k == c.
+        //
+        // Padding cells need no masks: their sigma' is 0 (tables), which
+        // makes every padded cell (i, j, k) <= the real cell
+        // (i, min(j, b), min(k, c)) of the same tile, and that cell comes
+        // first in row-major (= lexicographic) order, so it wins every tie.
+        // Tiles that hold no real cell of a lane are skipped for that lane.
+        constexpr int SC = 1 << SH;
+        const uint32_t g2s = Ops::splat(g2 * SC);
         int rb[LANES], cb[LANES];
-        bool cand[LANES], last[LANES];
-        bool anyc = false;
+        bool full[LANES], face[LANES];
+        bool anyfull = false, anyface = false;
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
           rb[l] = LS(l, kLenB) - LS(l, kOrgJ) - j0;  // rows P-1 <= rb are real
           cb[l] = LS(l, kLenC) - LS(l, kOrgK) - k0;
-          last[l] = si[l] == la[l];
           const bool inside = !(flags[l] & kDone) && si[l] <= la[l] && rb[l] >= 0 && cb[l] >= 0;
-          cand[l] = MODE == kLocal ? inside : inside && (last[l] || rb[l] < N || cb[l] < N);
-          anyc |= cand[l];
+          full[l] = inside && (MODE == kLocal || si[l] == la[l]);
+          face[l] = MODE == kSemi && inside && !full[l] && (rb[l] < N || cb[l] < N);
+          anyfull |= full[l];
+          anyface |= face[l];
         }
-        auto keep_mask = [&](int P, int Q) -> uint32_t {
-          uint32_t m = 0;
-#pragma unroll
-          for (int l = 0; l < LANES; ++l) {
-            const bool in = cand[l] && P - 1 <= rb[l] && Q - 1 <= cb[l];
-            const bool face = MODE == kLocal || last[l] || P - 1 == rb[l] || Q - 1 == cb[l];
-            if (in && face) m |= Ops::mask(l);
-          }
-          return m;
+        auto key_of = [](int mval, uint32_t lin) -> unsigned long long {
+          return (static_cast<unsigned long long>(static_cast<uint32_t>(mval) ^ 0x80000000u) << 32) |
+                 static_cast<unsigned long long>(0xFFFFFFFFu - lin);
         };
-        if (anyc) {
-          uint32_t stepmax = NEG;
+        auto lin_of = [&](int l, int P, int Q) -> uint32_t {
+          const uint32_t j = LS(l, kOrgJ) + j0 + P - 1, k = LS(l, kOrgK) + k0 + Q - 1;
+          return (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
+                     static_cast<uint32_t>(LS(l, kLenC) + 1) + k;
+        };
+        // Only a tile that can beat the item's best so far (its max value with
+        // the tile's smallest cell index) searches for its first maximal cell.
+        auto may_beat = [&](int l, int mval) -> bool {
+          const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(
+              &bkey[l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1))]);
+          return key_of(mval, lin_of(l, 1, 1)) > cur;
+        };
+        auto offer = [&](int l, int mval, int P, int Q) {
+          atomicMax(&bkey[l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1))], key_of(mval, lin_of(l, P, Q)));
+        };
+        // max over Q of Cu[P][Q] + g2 * (Q - 1) (Horner, one VIADDMNMX per cell)
+        auto row_max = [&](int P) -> uint32_t {
+          uint32_t acc = Cu[P][N];
 #pragma unroll
-          for (int P = 1; P <= N; ++P) {
-            uint32_t rowacc = NEG;
+          for (int Q = N - 1; Q >= 1; --Q) acc = Ops::addmax(acc, g2s, Cu[P][Q]);
+          return acc;
+        };
+        // max over P of Cu[P][Q] + g2 * (P - 1)
+        auto col_max = [&](int Q) -> uint32_t {
+          uint32_t acc = Cu[N][Q];
 #pragma unroll
-            for (int Q = 1; Q <= N; ++Q)
-              rowacc = Ops::addmax(lop_sel(NEG, Cu[P][Q], keep_mask(P, Q)), Ops::splat((g2 * (Q - 1)) << SH), rowacc);
-            stepmax = Ops::addmax(rowacc, Ops::splat((g2 * (P - 1)) << SH), stepmax);
-          }
+          for (int P = N - 1; P >= 1; --P) acc = Ops::addmax(acc, g2s, Cu[P][Q]);
+          return acc;
+        };
+        if (anyfull) {
+          uint32_t stepmax = row_max(N);
+#pragma unroll
+          for (int P = N - 1; P >= 1; --P) stepmax = Ops::addmax(stepmax, g2s, row_max(P));
 #pragma unroll
           for (int l = 0; l < LANES; ++l) {
-            if (!cand[l]) continue;
-            const int sm = Ops::lane(stepmax, l);
-            const int mval = (sm + ((g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0)) << SH)) >> SH;
-            if (!(flags[l] & kBestOk) || mval > LS(l, kBestV)) {
-              // first cell (row-major = lexicographic) attaining the maximum
-              int fp = 0, fq = 0;
-              bool found = false;
+            if (!full[l]) continue;
+            const int sm = Ops::lane(stepmax, l);  // scaled by SC, relative to the tile origin
+            const int mval = (sm >> SH) + g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
+            if (may_beat(l, mval)) {
+              // first row, then first cell of that row, attaining the maximum
+              int fp = 0;
 #pragma unroll
-              for (int P = 1; P <= N; ++P)
+              for (int P = N; P >= 1; --P)
+                if (Ops::lane(row_max(P), l) + g2 * SC * (P - 1) == sm) fp = P;
+              int fq = 0;
 #pragma unroll
-                for (int Q = 1; Q <= N; ++Q) {
-                  const int v = Ops::lane(lop_sel(NEG, Cu[P][Q], keep_mask(P, Q)), l) + ((g2 * (P - 1 + Q - 1)) << SH);
-                  if (!found && v == sm) {
-                    found = true;
-                    fp = P - 1;
-                    fq = Q - 1;
+              for (int P = 1; P <= N; ++P) {
+                if (P == fp) {
+#pragma unroll
+                  for (int Q = N; Q >= 1; --Q)
+                    if (Ops::lane(Cu[P][Q], l) + g2 * SC * (P - 1 + Q - 1) == sm) fq = Q;
+                }
+              }
+              offer(l, mval, fp, fq);
+            }
+          }
+        }
+        if constexpr (MODE == kSemi) {
+          if (anyface) {
+            // faces j == b (tile row rb) and k == c (tile column cb)
+#pragma unroll
+            for (int l = 0; l < LANES; ++l) {
+              if (!face[l]) continue;
+              const int base = g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
+              int fm = INT_MIN;
+              if (rb[l] < N) {
+#pragma unroll
+                for (int P = 1; P <= N; ++P)
+                  if (P - 1 == rb[l]) fm = (Ops::lane(row_max(P), l) >> SH) + g2 * (P - 1);
+              }
+              if (cb[l] < N) {
+#pragma unroll
+                for (int Q = 1; Q <= N; ++Q)
+                  if (Q - 1 == cb[l]) fm = max(fm, (Ops::lane(col_max(Q), l) >> SH) + g2 * (Q - 1));
+              }
+              if (!may_beat(l, fm + base)) continue;
+              int bv = 0, bp = 0, bq = 0;
+              bool have = false;
+              if (rb[l] < N) {
+#pragma unroll
+                for (int P = 1; P <= N; ++P) {
+                  if (P - 1 == rb[l]) {
+#pragma unroll
+                    for (int Q = 1; Q <= N; ++Q) {
+                      const int v = (Ops::lane(Cu[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1);
+                      if (!have || v > bv) bv = v, bp = P, bq = Q, have = true;
+                    }
                   }
                 }
-              const uint32_t j = LS(l, kOrgJ) + j0 + fp, k = LS(l, kOrgK) + k0 + fq;
-              LS(l, kBestV) = mval;
-              LS(l, kBestLin) = static_cast<int32_t>(
-                  (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
-                      static_cast<uint32_t>(LS(l, kLenC) + 1) + k);
-              flags[l] |= kBestOk;
+              }
+              if (cb[l] < N) {
+#pragma unroll
+                for (int Q = 1; Q <= N; ++Q) {
+                  if (Q - 1 == cb[l]) {
+#pragma unroll
+                    for (int P = 1; P <= N; ++P) {
+                      const int v = (Ops::lane(Cu[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1);
+                      // row-major order between the two faces: smaller P first
+                      if (!have || v > bv || (v == bv && P < bp)) bv = v, bp = P, bq = Q, have = true;
+                    }
+                  }
+                }
+              }
+              offer(l, bv + base, bp, bq);
             }
           }
         }
@@ -754,11 +874,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         sw[l] = BLOCKS ? si[l] >= LS(l, kLen) : si[l] > la[l];
         if (sw[l]) {
           if constexpr (MODE != kGlobal) {
-            if (flags[l] & kBestOk) {
-              const unsigned long long key =
-                  (static_cast<unsigned long long>(static_cast<uint32_t>(LS(l, kBestV)) ^ 0x80000000u) << 32) |
-                  static_cast<unsigned long long>(0xFFFFFFFFu - static_cast<uint32_t>(LS(l, kBestLin)));
-              atomicMax(args.out_key + LS(l, kTid), key);
+            // the last thread to leave the item publishes its best and frees the slot
+            const int slot = l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1));
+            __threadfence_block();
+            if (atomicAdd(&bcnt[slot], 1u) == static_cast<uint32_t>(T - 1)) {
+              __threadfence_block();
+              const unsigned long long key = atomicExch(&bkey[slot], 0ull);
+              if (key) atomicMax(args.out_key + LS(l, kTid), key);
+              bcnt[slot] = 0u;
             }
           }
         }
