@@ -66,12 +66,16 @@ struct DevBuf {
 
 struct BucketLaunch {
   int grid = 0, lanes = 0, mode = 0;
+  bool wave = false;
   ta::KernelEntry ke;
   int ctas = 0;
   DevBuf<int4> items;
   DevBuf<int32_t> soff, steps;
   DevBuf<int32_t> faces;
   DevBuf<int64_t> face_off;
+  DevBuf<int64_t> wave_base;  // wave mode: per triplet id, face area in 8-byte entries
+  int64_t face_bytes = 0;
+  uint32_t epoch = 0;         // wave mode: tag epoch of the last launch
   int64_t padded = 0;
 };
 
@@ -526,12 +530,142 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
   }
 }
 
+// Wave mode: the blocks of long triplets are spread over all CTAs instead of
+// running as one CTA's item sequence.  Blocks are ordered by anti-diagonal
+// d = J + K (a block depends only on blocks of diagonal d - 1), dealt
+// round-robin to the CTAs, and - with two lanes - paired only with a block it
+// cannot depend on (same diagonal, or another triplet) and of equal length, so
+// both lanes switch together.  With every CTA resident, the lowest unfinished
+// diagonal can always progress: no deadlock.  Faces travel through per-block
+// tagged rings (wavefront.cuh, WAVE).
+struct WavePlan {
+  std::vector<int4> items;
+  std::vector<int32_t> soff, steps;
+  std::vector<int64_t> base;  // per triplet id (only wave triplets set)
+  int64_t entries = 0;
+  int64_t padded_slices = 0;
+};
+
+void plan_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, const std::vector<int32_t>& b,
+               const std::vector<int32_t>& c, int max_ctas, int lanes, int grid, int64_t n, WavePlan* out,
+               int* ctas_out) {
+  struct Blk {
+    int d, id, J, K;
+  };
+  std::vector<Blk> blks;
+  out->base.assign(size_t(n), 0);
+  out->entries = 0;
+  for (int32_t id : ids) {
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+    out->base[size_t(id)] = out->entries;
+    out->entries += int64_t(bl.bj) * bl.bk * ta::wave_block_entries(a[size_t(id)], grid);
+    for (int J = 0; J < bl.bj; ++J)
+      for (int K = 0; K < bl.bk; ++K) blks.push_back(Blk{J + K, id, J, K});
+  }
+  std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.d < y.d; });
+  auto rec = [&](const Blk& x) {
+    const Blocks bl = blocks_of(b[size_t(x.id)], c[size_t(x.id)], grid);
+    return make_int4(x.id, (x.J << 16) | x.K, a[size_t(x.id)] + 1, (bl.bj << 16) | bl.bk);
+  };
+  std::vector<std::pair<int4, int4>> pairs;  // (lane 0, lane 1); lane 1 may be a null item
+  for (size_t i = 0; i < blks.size();) {
+    const int4 x = rec(blks[i]);
+    if (lanes == 2 && i + 1 < blks.size()) {
+      const Blk& u = blks[i];
+      const Blk& v = blks[i + 1];
+      const bool independent = u.id != v.id || u.d == v.d;
+      if (independent && a[size_t(u.id)] == a[size_t(v.id)]) {
+        pairs.push_back({x, rec(v)});
+        i += 2;
+        continue;
+      }
+    }
+    pairs.push_back({x, make_int4(-1, 0, x.z, 0x00010001)});
+    i += 1;
+  }
+  const int C = int(std::max<size_t>(1, std::min<size_t>(size_t(max_ctas), pairs.size())));
+  *ctas_out = C;
+  std::vector<std::vector<int4>> lists(size_t(C) * lanes);
+  std::vector<int64_t> load(size_t(C), 0);
+  for (size_t k = 0; k < pairs.size(); ++k) {
+    const size_t cta = k % size_t(C);
+    lists[cta * lanes].push_back(pairs[k].first);
+    if (lanes == 2) lists[cta * 2 + 1].push_back(pairs[k].second);
+    load[cta] += pairs[k].first.z;
+  }
+  out->items.clear();
+  out->soff.assign(size_t(C) * lanes + 1, 0);
+  out->steps.assign(size_t(C), 0);
+  out->padded_slices = 0;
+  for (size_t st = 0; st < lists.size(); ++st) {
+    out->soff[st] = int32_t(out->items.size());
+    for (const int4& it : lists[st]) {
+      out->items.push_back(it);
+      if (it.x >= 0) out->padded_slices += it.z;
+    }
+  }
+  out->soff[lists.size()] = int32_t(out->items.size());
+  for (int cta = 0; cta < C; ++cta) out->steps[size_t(cta)] = int32_t(load[size_t(cta)] + 2 * (grid - 1));
+}
+
+// Long triplets go to wave mode when there are too few of them to fill the
+// CTA lane streams (e.g. a single 1000-2000 bp triplet, config C5).
+bool wave_eligible(int32_t a, int32_t b, int32_t c, int grid) {
+  const Blocks bl = blocks_of(b, c, grid);
+  return grid == ta::kGridSizes[ta::kNumGrid - 1] && bl.bj * bl.bk > 1 && a + 1 < 65535;
+}
+
+void split_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, const std::vector<int32_t>& b,
+                const std::vector<int32_t>& c, int grid, int lane_streams, std::vector<int32_t>* wave,
+                std::vector<int32_t>* rest) {
+  wave->clear();
+  rest->clear();
+  std::vector<int32_t> cand;
+  for (int32_t id : ids)
+    (wave_eligible(a[size_t(id)], b[size_t(id)], c[size_t(id)], grid) ? cand : *rest).push_back(id);
+  if (int64_t(cand.size()) * 2 <= lane_streams) {
+    *wave = cand;
+  } else {
+    rest->insert(rest->end(), cand.begin(), cand.end());
+    std::sort(rest->begin(), rest->end());
+  }
+}
+
 // Host planning + upload for one bucket (outside any timed region).
 int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
-                   bool trace, cudaStream_t st, BucketLaunch* bl) {
+                   bool trace, cudaStream_t st, BucketLaunch* bl, bool wave = false) {
   bl->grid = grid;
   bl->lanes = lanes;
   bl->mode = mode;
+  bl->wave = wave;
+  if (wave) {
+    bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, 2);
+    const ta::KernelEntry& ke = bl->ke;
+    if (!ke.fn) return fail(TA_ERR_LOGIC, "no wave kernel instantiation for grid " + std::to_string(grid));
+    TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
+    int per_sm = 0;
+    TA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ke.fn, ke.threads, ke.smem));
+    if (per_sm < 1) return fail(TA_ERR_CUDA, "wavefront kernel does not fit on an SM");
+    WavePlan plan;
+    int ctas = 0;
+    plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, grid, int64_t(bt->a.size()), &plan, &ctas);
+    bl->ctas = ctas;
+    TA_CK(bl->items.reserve(plan.items.size()));
+    TA_CK(bl->soff.reserve(plan.soff.size()));
+    TA_CK(bl->steps.reserve(plan.steps.size()));
+    TA_CK(bl->faces.reserve(size_t(plan.entries) * 2 + 4));
+    TA_CK(bl->wave_base.reserve(plan.base.size()));
+    TA_CK(bl->face_off.reserve(1));
+    bl->face_bytes = plan.entries * 8;
+    TA_CK(cudaMemsetAsync(bl->faces.ptr, 0, size_t(bl->face_bytes), st));  // no stale tags
+    bl->epoch = 0;
+    TA_CK(cudaMemcpyAsync(bl->wave_base.ptr, plan.base.data(), plan.base.size() * 8, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
+    bl->padded = plan.padded_slices * grid * grid * ta::kTileN * ta::kTileN;
+    return TA_OK;
+  }
   bool multi = false;
   for (int32_t id : ids) {
     const Blocks b = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], grid);
@@ -540,7 +674,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
       break;
     }
   }
-  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, multi);
+  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, multi ? 1 : 0);
   const ta::KernelEntry& ke = bl->ke;
   if (!ke.fn) return fail(TA_ERR_LOGIC, "no kernel instantiation for grid " + std::to_string(grid));
   TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
@@ -572,6 +706,14 @@ int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st,
   args.cta_steps = bl->steps.ptr;
   args.faces = bl->faces.ptr;
   args.face_off = bl->face_off.ptr;
+  if (bl->wave) {
+    if (++bl->epoch >= 65536u) {  // tags would repeat: clear the rings
+      TA_CK(cudaMemsetAsync(bl->faces.ptr, 0, size_t(bl->face_bytes), st));
+      bl->epoch = 1;
+    }
+    args.wave_base = bl->wave_base.ptr;
+    args.epoch = bl->epoch;
+  }
   bl->ke.fn<<<bl->ctas, bl->ke.threads, bl->ke.smem, st>>>(args);
   TA_CK(cudaGetLastError());
   *launches += 1;
@@ -679,10 +821,17 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       bt->plan_key.clear();
       for (int gi = 0; gi < ta::kNumGrid; ++gi) {
         if (buckets[size_t(gi)].empty()) continue;
-        bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
-        if (int rc = prepare_bucket(bt, buckets[size_t(gi)], ta::kGridSizes[gi], lanes_of[size_t(gi)], opt.mode,
-                                    false, st, bt->plan_cache.back().get()))
-          return rc;
+        std::vector<int32_t> wave_ids, rest_ids;
+        split_wave(buckets[size_t(gi)], bt->a, bt->b, bt->c, ta::kGridSizes[gi], bt->ctx->sms * lanes_of[size_t(gi)],
+                   &wave_ids, &rest_ids);
+        for (int w = 0; w < 2; ++w) {
+          const std::vector<int32_t>& part = w ? wave_ids : rest_ids;
+          if (part.empty()) continue;
+          bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
+          if (int rc = prepare_bucket(bt, part, ta::kGridSizes[gi], lanes_of[size_t(gi)], opt.mode, false, st,
+                                      bt->plan_cache.back().get(), w == 1))
+            return rc;
+        }
       }
       bt->plan_key = key;
     }
@@ -961,11 +1110,18 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     std::vector<BucketLaunch*> launch_now;
     for (int gi = 0; gi < ta::kNumGrid && rc == TA_OK; ++gi) {
       if (buckets[size_t(gi)].empty()) continue;
-      keep.push_back(std::make_unique<BucketLaunch>());
       const int lanes = s16_ok(scheme, max_bound[gi]) ? 2 : 1;
-      rc = prepare_bucket(&shim, buckets[size_t(gi)], ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy,
-                          keep.back().get());
-      launch_now.push_back(keep.back().get());
+      std::vector<int32_t> wave_ids, rest_ids;
+      split_wave(buckets[size_t(gi)], shim.a, shim.b, shim.c, ta::kGridSizes[gi], ctx->sms * lanes, &wave_ids,
+                 &rest_ids);
+      for (int w = 0; w < 2 && rc == TA_OK; ++w) {
+        const std::vector<int32_t>& part = w ? wave_ids : rest_ids;
+        if (part.empty()) continue;
+        keep.push_back(std::make_unique<BucketLaunch>());
+        rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy, keep.back().get(),
+                            w == 1);
+        launch_now.push_back(keep.back().get());
+      }
     }
     if (rc != TA_OK) break;
     DevBuf<int32_t>* ids_buf = nullptr;

@@ -24,62 +24,84 @@ struct KernelEntry {
 };
 
 // lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace requires lanes == 1;
-// blocks (multi-block long-triplet support) exists for the largest grid only.
-KernelEntry kernel_g4(int lanes, int mode, bool trace, bool blocks);
-KernelEntry kernel_g8(int lanes, int mode, bool trace, bool blocks);
-KernelEntry kernel_g12(int lanes, int mode, bool trace, bool blocks);
-KernelEntry kernel_g16(int lanes, int mode, bool trace, bool blocks);
+// blk: 0 single-plane, 1 sequential multi-block items, 2 wave (multi-CTA)
+// blocks; blk > 0 exists for the largest grid only, blk == 2 without trace.
+KernelEntry kernel_g4(int lanes, int mode, bool trace, int blk);
+KernelEntry kernel_g8(int lanes, int mode, bool trace, int blk);
+KernelEntry kernel_g12(int lanes, int mode, bool trace, int blk);
+KernelEntry kernel_g16(int lanes, int mode, bool trace, int blk);
+KernelEntry kernel_g16_wave(int lanes, int mode);
 
-inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, bool blocks) {
+inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int blk) {
+  if (blk == 2) return (grid == 16 && !trace) ? kernel_g16_wave(lanes, mode) : KernelEntry{};
   switch (grid) {
-    case 4: return kernel_g4(lanes, mode, trace, blocks);
-    case 8: return kernel_g8(lanes, mode, trace, blocks);
-    case 12: return kernel_g12(lanes, mode, trace, blocks);
-    case 16: return kernel_g16(lanes, mode, trace, blocks);
+    case 4: return kernel_g4(lanes, mode, trace, blk);
+    case 8: return kernel_g8(lanes, mode, trace, blk);
+    case 12: return kernel_g12(lanes, mode, trace, blk);
+    case 16: return kernel_g16(lanes, mode, trace, blk);
   }
   return {};
 }
 
 }  // namespace ta
 
+#define TA_KERNEL_ENTRY(G, L, M, TR, BL) \
+  KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR, BL>, WaveSmem<kTileN, G, L>::bytes, G * G, G}
+
 #define TA_DEFINE_KERNEL_TABLE(G, WITH_BLOCKS)                                         \
   namespace ta {                                                                       \
-  template <int L, int M, bool TR, bool BL>                                            \
-  static KernelEntry entry_##G() {                                                     \
-    return KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR, BL>,                     \
-                       WaveSmem<kTileN, G, L>::bytes, G * G, G};                       \
-  }                                                                                    \
-  template <bool BL>                                                                   \
+  template <int BL>                                                                    \
   static KernelEntry pick_##G(int lanes, int mode, bool trace) {                       \
     if (trace) {                                                                       \
       if (lanes != 1) return {};                                                       \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<1, kGlobal, true, BL>();                        \
-        case kSemi: return entry_##G<1, kSemi, true, BL>();                            \
-        case kLocal: return entry_##G<1, kLocal, true, BL>();                          \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, true, BL);                 \
+        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, true, BL);                     \
+        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, true, BL);                   \
       }                                                                                \
       return {};                                                                       \
     }                                                                                  \
     if (lanes == 1) {                                                                  \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<1, kGlobal, false, BL>();                       \
-        case kSemi: return entry_##G<1, kSemi, false, BL>();                           \
-        case kLocal: return entry_##G<1, kLocal, false, BL>();                         \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, false, BL);                \
+        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, false, BL);                    \
+        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, false, BL);                  \
       }                                                                                \
     } else {                                                                           \
       switch (mode) {                                                                  \
-        case kGlobal: return entry_##G<2, kGlobal, false, BL>();                       \
-        case kSemi: return entry_##G<2, kSemi, false, BL>();                           \
-        case kLocal: return entry_##G<2, kLocal, false, BL>();                         \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 2, kGlobal, false, BL);                \
+        case kSemi: return TA_KERNEL_ENTRY(G, 2, kSemi, false, BL);                    \
+        case kLocal: return TA_KERNEL_ENTRY(G, 2, kLocal, false, BL);                  \
       }                                                                                \
     }                                                                                  \
     return {};                                                                         \
   }                                                                                    \
-  KernelEntry kernel_g##G(int lanes, int mode, bool trace, bool blocks) {              \
-    if (blocks) {                                                                      \
-      if constexpr (WITH_BLOCKS) return pick_##G<true>(lanes, mode, trace);            \
+  KernelEntry kernel_g##G(int lanes, int mode, bool trace, int blk) {                  \
+    if (blk == 1) {                                                                    \
+      if constexpr (WITH_BLOCKS) return pick_##G<1>(lanes, mode, trace);               \
       return {};                                                                       \
     }                                                                                  \
-    return pick_##G<false>(lanes, mode, trace);                                        \
+    if (blk != 0) return {};                                                           \
+    return pick_##G<0>(lanes, mode, trace);                                            \
+  }                                                                                    \
+  }
+
+#define TA_DEFINE_WAVE_TABLE(G)                                                        \
+  namespace ta {                                                                       \
+  KernelEntry kernel_g##G##_wave(int lanes, int mode) {                                \
+    if (lanes == 1) {                                                                  \
+      switch (mode) {                                                                  \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, false, 2);                 \
+        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, false, 2);                     \
+        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, false, 2);                   \
+      }                                                                                \
+    } else {                                                                           \
+      switch (mode) {                                                                  \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 2, kGlobal, false, 2);                 \
+        case kSemi: return TA_KERNEL_ENTRY(G, 2, kSemi, false, 2);                     \
+        case kLocal: return TA_KERNEL_ENTRY(G, 2, kLocal, false, 2);                   \
+      }                                                                                \
+    }                                                                                  \
+    return {};                                                                         \
   }                                                                                    \
   }

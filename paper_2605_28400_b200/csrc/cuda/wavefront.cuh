@@ -64,7 +64,18 @@ struct WaveArgs {
   uint32_t one;                            // == 1; keeps packed adds on the FMA pipe (IMAD)
   int32_t* __restrict__ faces;             // block-boundary faces of long triplets (int32 lane values)
   const int64_t* __restrict__ face_off;    // per stream, in words
+  const int64_t* __restrict__ wave_base;   // WAVE: per triplet, its face area in 8-byte entries
+  uint32_t epoch;                          // WAVE: launch epoch, high half of every face tag
 };
+
+// Wave mode (one long triplet spread over many CTAs): every block has its own
+// down / right face rings in global memory, [a + 1][G][kSegE] entries of
+// (value, tag) written with single 8-byte stores; tag = epoch << 16 | i + 1.
+// A consumer checks the tags it staged and re-reads (L2) until they match, so
+// cross-CTA block dependencies need no fences or flags (8-byte store
+// atomicity, as in NCCL's LL protocol).
+constexpr int kSegE = 12;  // entries per face segment (N + 1 <= 11 used), 96 B = 6 x 16 B
+__host__ __device__ inline int64_t wave_block_entries(int a, int g) { return int64_t(2) * (a + 1) * g * kSegE; }
 
 // Long triplets are split into row-major G*N x G*N blocks of the (j, k)
 // plane; block (J, K) receives its top face (row J*GN - 1, GN + 1 values
@@ -178,10 +189,10 @@ struct WaveSmem {
   static constexpr int XW = 2 * N + 1;
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
-  static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
+  static constexpr size_t kX = (size_t(2) * XW * (T + 1) * 4 + 15) / 16 * 16;
   static constexpr int kLaneFields = 12;                   // cold per-lane state
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
-  static constexpr size_t kStage = size_t(LANES) * 2 * G * (N + 1) * 4;  // prefetched block faces
+  static constexpr size_t kStage = size_t(LANES) * 2 * G * kSegE * 8;  // prefetched block faces (either layout)
   static constexpr size_t kBar = 16;                       // two mbarriers (mailbox parity)
   static constexpr int kSlots = 64;                        // open stream items per lane (ring)
   static constexpr size_t kBest = size_t(LANES) * kSlots * 12;  // per-item best key + finish count
@@ -193,8 +204,14 @@ struct WaveSmem {
 enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kUnused6, kUnused7, kOrgJ, kOrgK, kLen, kBk };
 
 // ---------------------------------------------------------------------------
-template <int N, int G, int LANES, int MODE, bool TRACE, bool BLOCKS>
+template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
 __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args) {
+  // BLK: 0 = every triplet fits one plane; 1 = long triplets as consecutive
+  // block items of one stream (faces via a per-stream buffer); 2 = wave mode
+  // (blocks of a triplet on different CTAs, tagged faces).
+  constexpr bool BLOCKS = BLK != 0;
+  constexpr bool WAVE = BLK == 2;
+  static_assert(N + 1 <= kSegE, "face segment too small");
   static_assert(!TRACE || LANES == 1, "direction cube uses int32 lanes");
   static_assert((N * N) % 4 == 0, "tile cells must group by 4");
   static_assert(N <= 15, "a tile row's codes must fit one 32-bit word");
@@ -299,8 +316,10 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   auto fetch = [&](int l, int it, int iend) -> LaneLoad {
     int id = -1, a_ = 0, b_ = -1, c_ = -1, len = 0x3FFFFFFF, J = 0, K = 0, Bj = 1, Bk = 1;
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
-    if (it < iend) {
-      const int4 rec = __ldg(args.items + it);
+    int4 rec = make_int4(-1, 0, 0x3FFFFFFF, 0x00010001);
+    if (it < iend) rec = __ldg(args.items + it);
+    if (rec.x < 0 && it < iend) len = rec.z;  // null item: the lane idles for len slices
+    if (rec.x >= 0) {
       id = rec.x;
       J = rec.y >> 16;
       K = rec.y & 0xFFFF;
@@ -326,7 +345,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
-    uint32_t f = id >= 0 ? 0u : kDone;
+    uint32_t f = (id >= 0 || it < iend) ? 0u : kDone;  // a null item keeps the lane alive
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
     if (id >= 0 && J > 0) f |= kInTop;
     if (id >= 0 && K > 0) f |= kInLeft;
@@ -496,6 +515,32 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
           for (int l = 0; l < LANES; ++l) {
             const bool ok = si[l] <= la[l];
+            if constexpr (WAVE) {
+              const uint32_t want = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
+              const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+              const int a1 = la[l] + 1;
+              const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+              // staged (value, tag) entry e of segment seg; re-read from L2 until fresh
+              auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
+                uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kSegE + e];
+                while (v.y != want) {
+                  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(src + e));
+                }
+                return static_cast<int32_t>(v.x);
+              };
+              if (r == 0 && (flags[l] & kInTop) && ok) {
+                const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kSegE;
+#pragma unroll
+                for (int q = 0; q <= N; ++q) Cu[0][q] = lop_sel(Cu[0][q], Ops::splat(take(cc, src, q) << SH), Ops::mask(l));
+              }
+              if (cc == 0 && (flags[l] & kInLeft) && ok) {
+                const uint64_t* src = fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE;
+#pragma unroll
+                for (int p = 0; p < N; ++p)
+                  Cu[p + 1][0] = lop_sel(Cu[p + 1][0], Ops::splat(take(G + r, src, p) << SH), Ops::mask(l));
+              }
+              continue;
+            }
             if (r == 0 && (flags[l] & kInTop) && ok) {
               const int32_t* st = stage + (l * 2 * G + cc) * (N + 1);
 #pragma unroll
@@ -598,7 +643,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int P = 1; P <= N; ++P) {
         uint32_t a1 = sig_row(tab1, P - 1);
         if constexpr (TRACE) a1 = a1 * 16u + kTagT2;
-        uint32_t fl = flrow;
+        [[maybe_unused]] uint32_t fl = flrow;
         if constexpr (MODE == kLocal) {
           if (P < N) flrow = fma_add(flrow, one, ag2s);
         }
@@ -627,7 +672,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::addmax(Cu[P - 1][Q], kTagT6, x);                // t6
           }
           if constexpr (MODE == kLocal) {
-            x = Ops::max2(x, fl);  // floor 0 (oracle.cpp:59)
+            x = Ops::addmax(fl, one ^ 1u, x);  // floor 0 (oracle.cpp:59); fused form, no s16x2 re-pack
             if (Q < N) fl = fma_add(fl, one, ag2s);
           }
           if constexpr (MODE == kGlobal || MODE == kSemi) {
@@ -666,6 +711,22 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const bool rt = cc == G - 1 && (flags[l] & kOutRight);
           if (!dn && !rt) continue;
           const int a1 = la[l] + 1;
+          if constexpr (WAVE) {
+            const uint32_t tag = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
+            uint64_t* fb = reinterpret_cast<uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+            const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+            if (dn) {  // down ring of this block: segment cc, entries q = 0..N (q = 0 is the corner)
+              uint2* d = reinterpret_cast<uint2*>(fb + ((int64_t(blk) * 2 * a1 + si[l]) * G + cc) * kSegE);
+#pragma unroll
+              for (int q = 0; q <= N; ++q) d[q] = make_uint2(static_cast<uint32_t>(Ops::lane(Cu[N][q], l) >> SH), tag);
+            }
+            if (rt) {  // right ring: segment r, entries p = 0..N-1
+              uint2* d = reinterpret_cast<uint2*>(fb + (((int64_t(blk) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
+#pragma unroll
+              for (int p = 0; p < N; ++p) d[p] = make_uint2(static_cast<uint32_t>(Ops::lane(Cu[p + 1][N], l) >> SH), tag);
+            }
+            continue;
+          }
           int32_t* fb = args.faces + args.face_off[sbase + l];
           if (dn) {  // Fdown[K][i][cN + q], q = 0 is the corner (k = cN - 1)
             int32_t* d = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
@@ -685,7 +746,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
       // ---- 6. direction cube slot (64 B per tile-slice) -----------------
       if constexpr (TRACE) {
-        if (!(flags[0] & kDone) && si[0] <= la[0]) {
+        if (!(flags[0] & kDone) && si[0] <= la[0] && LS(0, kTid) >= 0) {
           const int a1 = la[0] + 1;
           const int blk = (LS(0, kOrgJ) / GN) * LS(0, kBk) + LS(0, kOrgK) / GN;
           uint4* dst = args.dirs + args.dir_off[LS(0, kTid)] + ((size_t(blk) * a1 + si[0]) * T + tile) * 4;
@@ -931,6 +992,24 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int l = 0; l < LANES; ++l) {
         if ((flags[l] & kDone) || si[l] > la[l]) continue;
         const int a1 = la[l] + 1;
+        if constexpr (WAVE) {
+          const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+          const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+          auto fetch_seg = [&](int seg, const uint64_t* src) {
+            uint64_t* dst = reinterpret_cast<uint64_t*>(stage) + (l * 2 * G + seg) * kSegE;
+#pragma unroll
+            for (int v = 0; v < kSegE / 2; ++v)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                               static_cast<uint32_t>(__cvta_generic_to_shared(dst + 2 * v))),
+                           "l"(src + 2 * v)
+                           : "memory");
+          };
+          if (r == 0 && (flags[l] & kInTop))  // down ring of block (J - 1, K), segment cc
+            fetch_seg(cc, fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kSegE);
+          if (cc == 0 && (flags[l] & kInLeft))  // right ring of block (J, K - 1), segment r
+            fetch_seg(G + r, fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
+          continue;
+        }
         const int32_t* fb = args.faces + args.face_off[sbase + l];
         if (r == 0 && (flags[l] & kInTop)) {
           const int32_t* src = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
