@@ -57,7 +57,33 @@ class Oracle:
         L.to_rng_next.restype = u64
         L.to_sigma.argtypes = [ctypes.c_char, ctypes.c_char, _Scheme]
         L.to_sop.argtypes = [ctypes.c_char, ctypes.c_char, ctypes.c_char, _Scheme]
+        L.to_affine_align.argtypes = [ctypes.c_char_p, i32, ctypes.c_char_p, i32, ctypes.c_char_p, i32,
+                                      _Scheme, i32, ctypes.c_int, u64, ctypes.POINTER(_Result),
+                                      ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]
+        L.to_affine_rescore.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, i32, i32, _Scheme, i32]
+        L.to_affine_rescore.restype = i32
         self.L = L
+
+    def affine(self, t: Sequence[str], scheme: Tuple[int, int, int, int], mode: int,
+               with_rows: bool = False, budget: int = 1 << 40) -> dict:
+        """SPEC-AFFINE.md alignment; scheme = (match, mismatch, gap, gap_open)."""
+        s0, s1, s2 = (x.encode() for x in t)
+        res = _Result()
+        cap = len(s0) + len(s1) + len(s2) + 1
+        rows = [ctypes.create_string_buffer(cap) for _ in range(3)] if with_rows else [None] * 3
+        rc = self.L.to_affine_align(s0, len(s0), s1, len(s1), s2, len(s2), _Scheme(*scheme[:3]), scheme[3],
+                                    mode, budget, ctypes.byref(res), *rows)
+        if rc:
+            return {"error": rc}
+        out = {"score": res.score, "end": [res.end_i, res.end_j, res.end_k]}
+        if with_rows:
+            out["begin"] = [res.begin_i, res.begin_j, res.begin_k]
+            out["rows"] = [rows[d].raw[:res.row_len].decode() for d in range(3)]
+        return out
+
+    def affine_rescore(self, rows, lo: int, hi: int, scheme) -> int:
+        r = [x.encode() for x in rows]
+        return self.L.to_affine_rescore(r[0], r[1], r[2], lo, hi, _Scheme(*scheme[:3]), scheme[3])
 
     def align(self, t: Sequence[str], scheme: Tuple[int, int, int], mode: int,
               with_rows: bool = False, budget: int = 1 << 40) -> dict:

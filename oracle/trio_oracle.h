@@ -80,6 +80,16 @@ int64_t to_generate(int spec_kind, int32_t p0, int32_t p1, int32_t p2, const int
 
 uint64_t to_rng_next(uint64_t seed, uint64_t stream, uint64_t counter);
 
+/* Affine-gap 3-way alignment as defined by SPEC-AFFINE.md (the reference has
+ * linear gaps only; affine_oracle.c).  open = gap_open <= 0; open = 0 is the
+ * reference linear model.  Same result / rows contract as to_oracle_align. */
+int to_affine_align(const char* s0, int32_t a, const char* s1, int32_t b, const char* s2, int32_t c,
+                    to_scheme s, int32_t open, int mode, uint64_t cell_budget, to_result* out, char* row0,
+                    char* row1, char* row2);
+/* SPEC-AFFINE.md column rule over columns [lo, hi) of three gapped rows. */
+int32_t to_affine_rescore(const char* r0, const char* r1, const char* r2, int32_t lo, int32_t hi, to_scheme s,
+                          int32_t open);
+
 #ifdef __cplusplus
 }
 #endif
