@@ -39,11 +39,14 @@ typedef enum {
 
 typedef enum { TA_GLOBAL = 0, TA_SEMIGLOBAL = 1, TA_LOCAL = 2 } ta_mode; /* core.hpp:48 */
 
-/* ScoringScheme (core.hpp:24-31): match > 0, mismatch <= 0, gap <= 0, |x| <= 1024. */
+/* ScoringScheme (core.hpp:24-31): match > 0, mismatch <= 0, gap <= 0, |x| <= 1024.
+ * gap_open (<= 0) is NOT in the reference (linear gaps only):
+ * it selects the affine model of SPEC-AFFINE.md; 0 = the reference model. */
 typedef struct {
   int32_t match;
   int32_t mismatch;
   int32_t gap;
+  int32_t gap_open;
 } ta_scheme;
 
 /* Engine knobs.  tile_size / team_width / team_threads mirror EngineConfig
@@ -60,6 +63,8 @@ typedef struct {
   int32_t team_threads;  /* EngineConfig::team_threads, >= 1 */
   int32_t lane_mode;     /* 0 Single32, 1 PackedDual16 (results identical; GPU picks lanes) */
   uint64_t cell_budget;
+  int32_t gap_model;     /* 0: affine kernels iff gap_open != 0; 1: always the affine kernels
+                            (with gap_open = 0 they reproduce the linear results) */
 } ta_options;
 
 /* Per-triplet results, caller-allocated, n entries each (ends/begins: 3n). */

@@ -93,14 +93,15 @@ def _raise(code: int, msg: str):
 # C-ABI binding
 
 class _Scheme(ctypes.Structure):
-    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap", ctypes.c_int32)]
+    _fields_ = [("match", ctypes.c_int32), ("mismatch", ctypes.c_int32), ("gap", ctypes.c_int32),
+                ("gap_open", ctypes.c_int32)]
 
 
 class _Options(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int32), ("with_rows", ctypes.c_int32),
                 ("tile_size", ctypes.c_int32), ("team_width", ctypes.c_int32),
                 ("team_threads", ctypes.c_int32), ("lane_mode", ctypes.c_int32),
-                ("cell_budget", ctypes.c_uint64)]
+                ("cell_budget", ctypes.c_uint64), ("gap_model", ctypes.c_int32)]
 
 
 class _Results(ctypes.Structure):
@@ -194,6 +195,7 @@ class ScoringScheme:
     match: int = 1
     mismatch: int = -1
     gap: int = -2
+    gap_open: int = 0  # not in the reference: affine model of SPEC-AFFINE.md (0 = linear)
 
     def validate(self) -> None:  # core.cpp:10-18
         if self.match <= 0:
@@ -204,9 +206,13 @@ class ScoringScheme:
             raise InvalidArgument("gap score must be <= 0")
         if max(abs(self.match), abs(self.mismatch), abs(self.gap)) > 1024:
             raise InvalidArgument("score magnitudes must be <= 1024")
+        if self.gap_open > 0:
+            raise InvalidArgument("gap open score must be <= 0")
+        if abs(self.gap_open) > 1024:
+            raise InvalidArgument("score magnitudes must be <= 1024")
 
     def _c(self) -> _Scheme:
-        return _Scheme(self.match, self.mismatch, self.gap)
+        return _Scheme(self.match, self.mismatch, self.gap, self.gap_open)
 
 
 def make_scheme(match: int, mismatch: int, gap: int) -> ScoringScheme:
@@ -292,6 +298,7 @@ class EngineConfig:  # tiled.hpp:18-30
     lane_mode: LaneMode = LaneMode.Single32
     cell_budget: int = K_ENGINE_CELL_BUDGET
     team_threads: int = 1
+    gap_model: int = 0  # 1: force the affine kernels (SPEC-AFFINE.md) even when gap_open == 0
 
     def validate(self) -> None:  # tiled.cpp:8-15
         if self.tile_size < 1 or self.tile_size > 4096:
@@ -377,7 +384,7 @@ def _options(mode, with_rows, cfg: Optional[EngineConfig], cell_budget=None) -> 
     cfg = cfg or EngineConfig()
     budget = cfg.cell_budget if cell_budget is None else cell_budget
     return _Options(int(mode), int(bool(with_rows)), cfg.tile_size, cfg.team_width, cfg.team_threads,
-                    int(cfg.lane_mode), budget)
+                    int(cfg.lane_mode), budget, int(cfg.gap_model))
 
 
 def align_arrays(seqs: np.ndarray, offsets: np.ndarray, scheme: ScoringScheme,

@@ -25,6 +25,7 @@
 
 #include "../../../include/trioalign_capi.h"
 #include "kernels.h"
+#include "kernels_aff.h"
 
 namespace {
 
@@ -244,6 +245,93 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
   }
 }
 
+// K3a: traceback walker of the affine path (SPEC-AFFINE.md).  Each cell
+// record (affine.cuh) holds the 3-bit tags of V1's source (7 = start), of
+// B's argmax and of the predecessor type of every V_t; tag = 7 - type.
+__global__ void affine_walker_kernel(const ta::TripletDesc* __restrict__ desc, const uint32_t* __restrict__ seq,
+                                     const int32_t* __restrict__ ids, int n, const uint32_t* __restrict__ dirs,
+                                     const int64_t* __restrict__ dir_off, int mode, const int32_t* __restrict__ end,
+                                     int32_t* __restrict__ begin, char* __restrict__ rows,
+                                     const int64_t* __restrict__ row_off, int32_t* __restrict__ row_len,
+                                     int32_t* __restrict__ status) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int id = ids[x];
+  const ta::TripletDesc d = desc[id];
+  constexpr int N = ta::kAffN, G = ta::kAffG, T = G * G, GN = G * N;
+  const uint32_t* base = dirs + dir_off[id] * 4;
+  const int Bk = (d.c + 1 + GN - 1) / GN;
+  auto rec_at = [&](int i, int j, int k) -> uint32_t {
+    const int blk = (j / GN) * Bk + (k / GN);
+    const int jj = j % GN, kk = k % GN;
+    const int t = (jj / N) * G + (kk / N);
+    const int cell = (jj % N) * N + (kk % N);
+    return base[((int64_t(blk) * (d.a + 1) + i) * T + t) * ta::kAffRec + cell];
+  };
+  static constexpr int kMaskOf[8] = {0, 7, 3, 5, 6, 1, 2, 4};
+  const int ei = end[3 * id], ej = end[3 * id + 1], ek = end[3 * id + 2];
+  // pass 1: path length and begin
+  int i = ei, j = ej, k = ek, steps = 0;
+  int ty = 7 - int((rec_at(i, j, k) >> 3) & 7u);
+  const int t_end = ty;
+  const int limit = d.a + d.b + d.c + 1;
+  bool ok = true;
+  for (;;) {
+    const uint32_t rc = rec_at(i, j, k);
+    if (ty == 1 && (rc & 7u) == 7u) break;  // a start
+    const uint32_t tag = ty == 1 ? (rc & 7u) : (rc >> (6 + 3 * (ty - 2))) & 7u;
+    const int m = kMaskOf[ty];
+    const int di = m & 1, dj = (m >> 1) & 1, dk = (m >> 2) & 1;
+    if (tag == 7u || i - di < 0 || j - dj < 0 || k - dk < 0 || ++steps > limit) {
+      ok = false;
+      break;
+    }
+    i -= di, j -= dj, k -= dk;
+    ty = 7 - int(tag);
+  }
+  if (!ok) {
+    status[id] = TA_ERR_LOGIC;
+    row_len[id] = 0;
+    return;
+  }
+  begin[3 * id] = i, begin[3 * id + 1] = j, begin[3 * id + 2] = k;
+  const int bi = i, bj = j, bk = k;
+  const bool semi = mode == ta::kSemi;
+  const int prefix = semi ? (bi + bj + bk) : 0;
+  const int suffix = semi ? ((d.a - ei) + (d.b - ej) + (d.c - ek)) : 0;
+  row_len[id] = prefix + steps + suffix;
+  const int64_t cap = int64_t(d.a) + d.b + d.c;
+  char* r0 = rows + row_off[id];
+  char* r1 = r0 + cap;
+  char* r2 = r1 + cap;
+  int pos = 0;
+  if (semi) {
+    for (int p = 0; p < bi; ++p, ++pos) r0[pos] = base_char(seq, d.w0, p), r1[pos] = '-', r2[pos] = '-';
+    for (int p = 0; p < bj; ++p, ++pos) r0[pos] = '-', r1[pos] = base_char(seq, d.w1, p), r2[pos] = '-';
+    for (int p = 0; p < bk; ++p, ++pos) r0[pos] = '-', r1[pos] = '-', r2[pos] = base_char(seq, d.w2, p);
+  }
+  // pass 2: the path columns back to front
+  i = ei, j = ej, k = ek, ty = t_end;
+  for (int s = steps - 1; s >= 0; --s) {
+    const uint32_t rc = rec_at(i, j, k);
+    const uint32_t tag = ty == 1 ? (rc & 7u) : (rc >> (6 + 3 * (ty - 2))) & 7u;
+    const int m = kMaskOf[ty];
+    const int u0 = m & 1, u1 = (m >> 1) & 1, u2 = (m >> 2) & 1;
+    const int at = prefix + s;
+    r0[at] = u0 ? base_char(seq, d.w0, i - 1) : '-';
+    r1[at] = u1 ? base_char(seq, d.w1, j - 1) : '-';
+    r2[at] = u2 ? base_char(seq, d.w2, k - 1) : '-';
+    i -= u0, j -= u1, k -= u2;
+    ty = 7 - int(tag);
+  }
+  pos = prefix + steps;
+  if (semi) {
+    for (int p = ei; p < d.a; ++p, ++pos) r0[pos] = base_char(seq, d.w0, p), r1[pos] = '-', r2[pos] = '-';
+    for (int p = ej; p < d.b; ++p, ++pos) r0[pos] = '-', r1[pos] = base_char(seq, d.w1, p), r2[pos] = '-';
+    for (int p = ek; p < d.c; ++p, ++pos) r0[pos] = '-', r1[pos] = '-', r2[pos] = base_char(seq, d.w2, p);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // per-device context (stream + events), created lazily
 
@@ -320,6 +408,9 @@ int validate_scheme(const ta_scheme& s) {
   if (s.gap > 0) return fail(TA_ERR_INVALID_ARGUMENT, "gap score must be <= 0");
   if (std::abs(s.match) > 1024 || std::abs(s.mismatch) > 1024 || std::abs(s.gap) > 1024)
     return fail(TA_ERR_INVALID_ARGUMENT, "score magnitudes must be <= 1024");
+  // affine extension (SPEC-AFFINE.md)
+  if (s.gap_open > 0) return fail(TA_ERR_INVALID_ARGUMENT, "gap open score must be <= 0");
+  if (std::abs(s.gap_open) > 1024) return fail(TA_ERR_INVALID_ARGUMENT, "score magnitudes must be <= 1024");
   return TA_OK;
 }
 
@@ -400,6 +491,7 @@ struct ta_batch {
   // score-path launch plans of the last run (reused while the bucket
   // contents, lanes and mode are unchanged)
   std::vector<std::unique_ptr<BucketLaunch>> plan_cache;
+  std::vector<ta::AffEntry> aff_cache;  // affine path: kernel per cached plan
   std::string plan_key;
   int last_mode = -1;
   bool last_rows = false;
@@ -423,8 +515,8 @@ struct Blocks {
   int bj = 1, bk = 1;
 };
 
-inline Blocks blocks_of(int32_t b, int32_t c, int grid) {
-  const int gn = grid * ta::kTileN;
+inline Blocks blocks_of(int32_t b, int32_t c, int grid, int tile_n = ta::kTileN) {
+  const int gn = grid * tile_n;
   return Blocks{(b + 1 + gn - 1) / gn, (c + 1 + gn - 1) / gn};
 }
 
@@ -444,22 +536,22 @@ inline int item_len(int32_t a, const Blocks& bl, int grid) {
 // a long triplet contributes its Bj*Bk blocks as consecutive items.
 void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a,
                   const std::vector<int32_t>& b, const std::vector<int32_t>& c, int ctas, int lanes, int grid,
-                  StreamPlan* out) {
+                  StreamPlan* out, int tile_n = ta::kTileN, bool affine = false) {
   const int S = ctas * lanes;
-  const int gn = grid * ta::kTileN;
+  const int gn = grid * tile_n;
   std::vector<std::vector<int32_t>> lists(static_cast<size_t>(S));
   std::vector<int64_t> load(static_cast<size_t>(S), 0), face(static_cast<size_t>(S), 0);
   using Load = std::pair<int64_t, int32_t>;
   auto cost = [&](int32_t id) {
-    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid, tile_n);
     return int64_t(item_len(a[size_t(id)], bl, grid)) * bl.bj * bl.bk;
   };
   auto put = [&](int s, int32_t id) {
     lists[size_t(s)].push_back(id);
     load[size_t(s)] += cost(id);
-    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid, tile_n);
     if (bl.bj * bl.bk > 1)
-      face[size_t(s)] = std::max(face[size_t(s)], ta::face_words(a[size_t(id)], bl.bk, gn));
+      face[size_t(s)] = std::max(face[size_t(s)], (affine ? ta::aff_face_words(a[size_t(id)], bl.bk, gn) : ta::face_words(a[size_t(id)], bl.bk, gn)));
   };
   std::vector<int32_t> singles;
   if (lanes == 2) {
@@ -469,7 +561,7 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
     // unpaired triplets at the stream tails.
     std::vector<int32_t> order(ids);
     auto key = [&](int32_t id) {
-      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid, tile_n);
       return std::make_tuple(item_len(a[size_t(id)], bl, grid), bl.bj, bl.bk);
     };
     std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return key(x) < key(y); });
@@ -515,7 +607,7 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
     out->face_off[size_t(s)] = out->face_words;
     out->face_words += face[size_t(s)];
     for (int32_t id : lists[size_t(s)]) {
-      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+      const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid, tile_n);
       const int len = item_len(a[size_t(id)], bl, grid);
       for (int J = 0; J < bl.bj; ++J)
         for (int K = 0; K < bl.bk; ++K) out->items.push_back(make_int4(id, (J << 16) | K, len, (bl.bj << 16) | bl.bk));
@@ -730,6 +822,219 @@ int launch_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int l
   return TA_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Affine path (SPEC-AFFINE.md): one 16 x 16 grid of 5 x 5 tiles; triplets
+// wider than 80 cells run as block items (faces of 4 values per position).
+
+// Largest biased, gap-shifted value: -8 open + (match - 2 gap) * (slices + extents).
+int64_t aff_lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c) {
+  const int g2 = 2 * s.gap;
+  const int64_t gn = ta::kAffExtent;
+  const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
+  const int warps = (ta::kAffG * ta::kAffG + 31) / 32;
+  const int64_t slices = std::max<int64_t>(a + 1, ta::kAffG + 2 + warps);
+  return -8 * int64_t(s.gap_open) + int64_t(s.match - g2) * (slices + ej + ek);
+}
+
+bool aff_s16_ok(const ta_scheme& s, int64_t max_bound) {
+  const int g2 = 2 * s.gap;
+  const int mp = s.match - g2, mm = s.mismatch - g2;
+  if (mm < 0 || mp > 127) return false;
+  return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kAffN + 2 * int64_t(-s.gap_open) <= 32000;
+}
+
+int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mode, bool trace, bool blocks,
+                cudaStream_t st, BucketLaunch* bl, ta::AffEntry* ae) {
+  *ae = ta::lookup_affine(lanes, mode, trace, blocks);
+  if (!ae->fn) return fail(TA_ERR_LOGIC, "no affine kernel instantiation");
+  TA_CK(cudaFuncSetAttribute(ae->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ae->smem)));
+  int per_sm = 0;
+  TA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ae->fn, ae->threads, ae->smem));
+  if (per_sm < 1) return fail(TA_ERR_CUDA, "affine kernel does not fit on an SM");
+  const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
+  bl->grid = ta::kAffG;
+  bl->lanes = lanes;
+  bl->mode = mode;
+  bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
+  StreamPlan plan;
+  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, ta::kAffG, &plan, ta::kAffN, true);
+  if (plan.face_words > (int64_t(1) << 31)) return fail(TA_ERR_CAPACITY, "block-face scratch exceeds 2^31 words");
+  TA_CK(bl->items.reserve(plan.items.size()));
+  TA_CK(bl->soff.reserve(plan.soff.size()));
+  TA_CK(bl->steps.reserve(plan.steps.size()));
+  TA_CK(bl->faces.reserve(size_t(plan.face_words) + 4));
+  TA_CK(bl->face_off.reserve(plan.face_off.size()));
+  TA_CK(cudaMemcpyAsync(bl->face_off.ptr, plan.face_off.data(), plan.face_off.size() * 8, cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
+  TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
+  bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * ta::kAffN * ta::kAffN;
+  return TA_OK;
+}
+
+int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base, cudaStream_t st,
+               int64_t* launches) {
+  ta::AffArgs args = base;
+  args.items = bl->items.ptr;
+  args.stream_off = bl->soff.ptr;
+  args.cta_steps = bl->steps.ptr;
+  args.faces = bl->faces.ptr;
+  args.face_off = bl->face_off.ptr;
+  ae.fn<<<bl->ctas, ae.threads, ae.smem, st>>>(args);
+  TA_CK(cudaGetLastError());
+  *launches += 1;
+  return TA_OK;
+}
+
+int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
+               const std::vector<int32_t>& all_ok, bool rows) {
+  const int64_t n = bt->n;
+  std::vector<int32_t> single, multi;
+  int64_t maxb = 0;
+  for (int32_t id : all_ok) {
+    const int32_t B = bt->b[size_t(id)], C = bt->c[size_t(id)];
+    (std::max(B, C) + 1 <= ta::kAffExtent ? single : multi).push_back(id);
+    maxb = std::max(maxb, aff_lane_bound(scheme, bt->a[size_t(id)], B, C));
+  }
+  const int lanes = (!rows && aff_s16_ok(scheme, maxb)) ? 2 : 1;
+  ta::AffArgs base{};
+  base.seq = bt->seq.ptr;
+  base.desc = bt->d_desc.ptr;
+  base.out_score = bt->d_score.ptr;
+  base.out_end = bt->d_end.ptr;
+  base.out_key = bt->d_key.ptr;
+  base.g2 = 2 * scheme.gap;
+  base.match_p = scheme.match - base.g2;
+  base.mismatch_p = scheme.mismatch - base.g2;
+  base.open = scheme.gap_open;
+  base.bias = -8 * scheme.gap_open;
+  base.one = 1u;
+  if (!bt->ev0) TA_CK(cudaEventCreate(&bt->ev0));
+  if (!bt->ev1) TA_CK(cudaEventCreate(&bt->ev1));
+  if (opt.mode != TA_GLOBAL) TA_CK(cudaMemsetAsync(bt->d_key.ptr, 0, size_t(n) * 8, st));
+  int64_t launches = 0;
+  int nbuckets = 0;
+  float ms = 0.f;
+  auto decode = [&](const std::vector<int32_t>& ids) -> int {
+    if (opt.mode == TA_GLOBAL || ids.empty()) return TA_OK;
+    TA_CK(bt->d_ids.reserve(ids.size()));
+    TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice, st));
+    const int64_t m = int64_t(ids.size());
+    decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr, m,
+                                                                bt->d_score.ptr, bt->d_end.ptr);
+    TA_CK(cudaGetLastError());
+    ++launches;
+    return TA_OK;
+  };
+  if (!rows) {
+    std::string key = "aff:" + std::to_string(opt.mode) + ":" + std::to_string(lanes) + ":" +
+                      std::to_string(scheme.gap_open) + ":" + std::to_string(all_ok.size());
+    uint64_t h = 1469598103934665603ull;
+    for (int32_t id : all_ok) h = (h ^ uint64_t(id)) * 1099511628211ull;
+    key += ":" + std::to_string(h);
+    if (key != bt->plan_key) {
+      bt->plan_cache.clear();
+      bt->aff_cache.clear();
+      bt->plan_key.clear();
+      for (int w = 0; w < 2; ++w) {
+        const std::vector<int32_t>& part = w ? multi : single;
+        if (part.empty()) continue;
+        bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
+        bt->aff_cache.emplace_back();
+        if (int rc = aff_prepare(bt, part, lanes, opt.mode, false, w == 1, st, bt->plan_cache.back().get(),
+                                 &bt->aff_cache.back()))
+          return rc;
+      }
+      bt->plan_key = key;
+    }
+    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
+      TA_CK(bt->d_ids.reserve(all_ok.size()));
+      TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, all_ok.data(), all_ok.size() * 4, cudaMemcpyHostToDevice, st));
+    }
+    TA_CK(cudaEventRecord(bt->ev0, st));
+    for (size_t x = 0; x < bt->plan_cache.size(); ++x) {
+      if (int rc = aff_launch(bt->plan_cache[x].get(), bt->aff_cache[x], base, st, &launches)) return rc;
+      bt->stats.padded_cells += bt->plan_cache[x]->padded;
+      ++nbuckets;
+    }
+    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
+      const int64_t m = int64_t(all_ok.size());
+      decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr, m,
+                                                                  bt->d_score.ptr, bt->d_end.ptr);
+      TA_CK(cudaGetLastError());
+      ++launches;
+    }
+    TA_CK(cudaEventRecord(bt->ev1, st));
+    TA_CK(cudaEventSynchronize(bt->ev1));
+    TA_CK(cudaEventElapsedTime(&ms, bt->ev0, bt->ev1));
+  } else {
+    // records: (a+1) * blocks * T tile-slices of kAffRec words per triplet, chunked by free HBM
+    size_t free_b = 0, total_b = 0;
+    TA_CK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b) * 0.5));
+    bt->plan_key.clear();
+    TA_CK(cudaEventRecord(bt->ev0, st));
+    for (int w = 0; w < 2; ++w) {
+      const std::vector<int32_t>& ids = w ? multi : single;
+      if (ids.empty()) continue;
+      ++nbuckets;
+      size_t pos = 0;
+      while (pos < ids.size()) {
+        std::vector<int32_t> chunk;
+        std::vector<int64_t> diroff(static_cast<size_t>(n), 0);
+        size_t used = 0;  // uint4 units
+        while (pos < ids.size()) {
+          const int32_t id = ids[pos];
+          const Blocks blk = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], ta::kAffG, ta::kAffN);
+          const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * ta::kAffG * ta::kAffG *
+                              (ta::kAffRec / 4);
+          if (!chunk.empty() && (used + need) * 16 > budget) break;
+          diroff[size_t(id)] = int64_t(used);
+          used += need;
+          chunk.push_back(id);
+          ++pos;
+        }
+        TA_CK(bt->d_dirs.reserve(used));
+        TA_CK(bt->d_diroff.reserve(size_t(n)));
+        TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+        ta::AffArgs args = base;
+        args.dirs = reinterpret_cast<uint32_t*>(bt->d_dirs.ptr);
+        args.dir_off = bt->d_diroff.ptr;
+        BucketLaunch bl;
+        ta::AffEntry ae;
+        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1, st, &bl, &ae)) return rc;
+        if (int rc = aff_launch(&bl, ae, args, st, &launches)) return rc;
+        bt->stats.padded_cells += bl.padded;
+        if (int rc = decode(chunk)) return rc;
+        TA_CK(bt->d_ids.reserve(chunk.size()));
+        TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
+        const int m = int(chunk.size());
+        affine_walker_kernel<<<unsigned((m + 127) / 128), 128, 0, st>>>(
+            bt->d_desc.ptr, bt->seq.ptr, bt->d_ids.ptr, m, reinterpret_cast<const uint32_t*>(bt->d_dirs.ptr),
+            bt->d_diroff.ptr, opt.mode, bt->d_end.ptr, bt->d_begin.ptr, bt->d_rows.ptr, bt->d_rowoff.ptr,
+            bt->d_rowlen.ptr, bt->d_status.ptr);
+        TA_CK(cudaGetLastError());
+        ++launches;
+        TA_CK(cudaStreamSynchronize(st));  // bl's buffers die here
+      }
+    }
+    TA_CK(cudaEventRecord(bt->ev1, st));
+    TA_CK(cudaEventSynchronize(bt->ev1));
+    TA_CK(cudaEventElapsedTime(&ms, bt->ev0, bt->ev1));
+  }
+  int64_t cells = 0;
+  for (int32_t id : all_ok) cells += int64_t(bt->a[size_t(id)]) * bt->b[size_t(id)] * bt->c[size_t(id)];
+  bt->stats.kernel_ms = ms;
+  bt->stats.wavefront_ms = ms;
+  bt->stats.cells = cells;
+  bt->stats.launches = launches;
+  bt->stats.lanes = lanes;
+  bt->stats.buckets = nbuckets;
+  bt->last_mode = opt.mode;
+  bt->last_rows = rows;
+  return TA_OK;
+}
+
 int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
              ta_results* rows_out) {
   const int64_t n = bt->n;
@@ -784,6 +1089,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     all_ok.push_back(int32_t(t));
   }
   if (cfg_rc) g_err = cfg_msg;
+  if (scheme.gap_open != 0 || opt.gap_model == 1) return run_affine(bt, scheme, opt, st, all_ok, rows);
 
   ta::WaveArgs base{};
   base.seq = bt->seq.ptr;
@@ -1318,7 +1624,8 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
                    const ta_scheme* scheme, const ta_options* opt, ta_results* out, void* stream) {
   if (!scheme || !opt || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
   if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
-  if (!opt->with_rows && n > 0) {
+  const bool affine = scheme->gap_open != 0 || opt->gap_model == 1;
+  if (!opt->with_rows && n > 0 && !affine) {
     DeviceCtx* ctx = nullptr;
     if (int rc = get_ctx(device, &ctx)) return rc;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;

@@ -1,0 +1,62 @@
+// kernels_aff.h — instantiation table of the affine-gap wavefront kernel
+// (affine.cuh): one 16 x 16 grid of 5 x 5 tiles (80-cell block side).
+#pragma once
+
+#include <cstddef>
+
+#include "affine.cuh"
+
+namespace ta {
+
+constexpr int kAffG = 16;
+constexpr int kAffExtent = kAffG * kAffN;
+
+using AffFn = void (*)(AffArgs);
+
+struct AffEntry {
+  AffFn fn = nullptr;
+  size_t smem = 0;
+  int threads = 0;
+};
+
+// trace requires lanes == 1
+AffEntry affine_kernel_single(int lanes, int mode, bool trace);
+AffEntry affine_kernel_blocks(int lanes, int mode, bool trace);
+
+inline AffEntry lookup_affine(int lanes, int mode, bool trace, bool blocks) {
+  return blocks ? affine_kernel_blocks(lanes, mode, trace) : affine_kernel_single(lanes, mode, trace);
+}
+
+}  // namespace ta
+
+#define TA_AFF_ENTRY(L, M, TR, BL) \
+  AffEntry{&affine_kernel<kAffN, kAffG, L, M, TR, BL>, AffSmem<kAffN, kAffG, L>::bytes, kAffG * kAffG}
+
+#define TA_DEFINE_AFF_TABLE(NAME, BL)                          \
+  namespace ta {                                               \
+  AffEntry NAME(int lanes, int mode, bool trace) {             \
+    if (trace) {                                               \
+      if (lanes != 1) return {};                               \
+      switch (mode) {                                          \
+        case kGlobal: return TA_AFF_ENTRY(1, kGlobal, true, BL); \
+        case kSemi: return TA_AFF_ENTRY(1, kSemi, true, BL);     \
+        case kLocal: return TA_AFF_ENTRY(1, kLocal, true, BL);   \
+      }                                                        \
+      return {};                                               \
+    }                                                          \
+    if (lanes == 1) {                                          \
+      switch (mode) {                                          \
+        case kGlobal: return TA_AFF_ENTRY(1, kGlobal, false, BL); \
+        case kSemi: return TA_AFF_ENTRY(1, kSemi, false, BL);     \
+        case kLocal: return TA_AFF_ENTRY(1, kLocal, false, BL);   \
+      }                                                        \
+    } else {                                                   \
+      switch (mode) {                                          \
+        case kGlobal: return TA_AFF_ENTRY(2, kGlobal, false, BL); \
+        case kSemi: return TA_AFF_ENTRY(2, kSemi, false, BL);     \
+        case kLocal: return TA_AFF_ENTRY(2, kLocal, false, BL);   \
+      }                                                        \
+    }                                                          \
+    return {};                                                 \
+  }                                                            \
+  }

@@ -31,7 +31,7 @@ int32_t derive_team_width(int32_t tile_size, int32_t b, int32_t c) {
 }
 
 int64_t packed_score_bound(const Triplet& t, const ScoringScheme& scheme) {
-  const ta_scheme s{scheme.match, scheme.mismatch, scheme.gap};
+  const ta_scheme s{scheme.match, scheme.mismatch, scheme.gap, scheme.gap_open};
   return ta_packed_score_bound(int64_t(t.s0.size()), int64_t(t.s1.size()), int64_t(t.s2.size()), &s);
 }
 
@@ -106,7 +106,7 @@ BatchOut run_engine(const std::vector<const Triplet*>& ts, const ScoringScheme& 
     }
   }
   offs.push_back(int64_t(seqs.size()));
-  const ta_scheme sch{scheme.match, scheme.mismatch, scheme.gap};
+  const ta_scheme sch{scheme.match, scheme.mismatch, scheme.gap, scheme.gap_open};
   ta_options opt{};
   opt.mode = int32_t(mode);
   opt.with_rows = rows ? 1 : 0;
@@ -115,6 +115,7 @@ BatchOut run_engine(const std::vector<const Triplet*>& ts, const ScoringScheme& 
   opt.team_threads = cfg.team_threads;
   opt.lane_mode = cfg.lane_mode == LaneMode::PackedDual16 ? 1 : 0;
   opt.cell_budget = rows ? rows_budget : cfg.cell_budget;
+  opt.gap_model = cfg.gap_model;
   ta_results res{};
   res.scores = out.score.data();
   res.ends = out.end.data();

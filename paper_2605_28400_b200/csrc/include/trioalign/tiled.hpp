@@ -20,6 +20,7 @@ struct EngineConfig {
   uint64_t cell_budget = uint64_t{1} << 31;  // max a*b*c per triplet (CapacityError)
   int32_t team_threads = 1;
   int32_t device = 0;                        // CUDA device (B200 extension)
+  int32_t gap_model = 0;                     // 1: always the affine kernels (B200 extension)
   void validate() const;                     // ConfigError (tiled.cpp:8-15)
 };
 

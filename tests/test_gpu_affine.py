@@ -1,0 +1,125 @@
+"""GPU parity of the affine-gap kernels (affine.cuh) through the C-ABI.
+
+The reference has linear gaps only, so (SPEC-AFFINE.md):
+* with gap_open = 0 the affine kernels (forced with gap_model = 1) must
+  reproduce the reference's own golden vectors - scores, ends and rows;
+* with gap_open < 0 they must equal the builder's affine oracle
+  (oracle/affine_oracle.c, pinned by tests/test_affine_oracle.py) bit for bit:
+  score, end, begin and rows, in every mode, for s16x2 and int32 lanes,
+  single-block and multi-block (long) triplets.
+Needs a B200."""
+import numpy as np
+import pytest
+
+import paper_2605_28400_b200 as ta
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+MODES = (0, 1, 2)
+
+
+def trips_to_arrays(trips):
+    parts, offs, pos = [], [0], 0
+    for t in trips:
+        for s in t:
+            parts.append(s.encode())
+            pos += len(s)
+            offs.append(pos)
+    return np.frombuffer(b"".join(parts) + b"\0", np.uint8), np.asarray(offs, np.int64)
+
+
+def run(trips, sch, mode, rows=False, force=False):
+    seqs, offs = trips_to_arrays(trips)
+    cfg = ta.EngineConfig(cell_budget=1 << 40, gap_model=1 if force else 0)
+    return ta.align_arrays(seqs, offs, ta.ScoringScheme(*sch), ta.AlignmentMode(mode), cfg=cfg,
+                           with_rows=rows, cell_budget=(1 << 40) if rows else None)
+
+
+def rand_trips(rng, n, lo, hi):
+    return [tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=int(L))) for L in rng.integers(lo, hi, size=3))
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_open_zero_reproduces_reference_golden(gpu_engine, mode):
+    cases = [c for c in load_golden("small_rows.json.gz") if c["mode"] == mode]
+    by_scheme = {}
+    for c in cases:
+        by_scheme.setdefault(tuple(c["scheme"]), []).append(c)
+    for sch, cs in by_scheme.items():
+        trips = [c["t"] for c in cs]
+        sc = run(trips, sch + (0,), mode, force=True)
+        rw = run(trips, sch + (0,), mode, rows=True, force=True)
+        for x, c in enumerate(cs):
+            want = c["oracle"]
+            assert int(sc["status"][x]) == 0 and int(rw["status"][x]) == 0
+            assert int(sc["score"][x]) == want["score"] and list(sc["end"][x]) == want["end"], (sch, c["t"])
+            assert int(rw["score"][x]) == want["score"] and list(rw["end"][x]) == want["end"], (sch, c["t"])
+            assert list(rw["begin"][x]) == want["begin"], (sch, c["t"])
+            assert list(rw["rows"][x]) == want["rows"], (sch, c["t"])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_affine_scores_vs_oracle(gpu_engine, oracle, mode):
+    rng = np.random.default_rng(300 + mode)
+    schemes = [(1, -1, -2, -3), (2, -1, -1, -4), (1, 0, 0, -2), (5, -4, -1, -6), (7, -30, -20, -40), (1, -1, -2, -1)]
+    for sch in schemes:
+        trips = rand_trips(rng, 40, 0, 70) + rand_trips(rng, 8, 70, 170)
+        out = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.affine(t, sch, mode)
+            assert int(out["status"][x]) == 0
+            assert int(out["score"][x]) == want["score"], (sch, mode, [len(s) for s in t])
+            assert list(out["end"][x]) == want["end"], (sch, mode, [len(s) for s in t])
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_affine_rows_vs_oracle(gpu_engine, oracle, mode):
+    rng = np.random.default_rng(400 + mode)
+    for sch in [(1, -1, -2, -3), (2, -1, -1, -5), (3, -2, -1, -1)]:
+        trips = rand_trips(rng, 30, 0, 50) + rand_trips(rng, 4, 75, 130)
+        trips += [("", "", ""), ("A", "", ""), ("", "ACGT", "TTTT"), ("T" * 90, "", "A" * 85)]
+        out = run(trips, sch, mode, rows=True)
+        for x, t in enumerate(trips):
+            want = oracle.affine(t, sch, mode, with_rows=True)
+            assert int(out["status"][x]) == 0, (sch, mode, x)
+            got = {"score": int(out["score"][x]), "end": list(out["end"][x]), "begin": list(out["begin"][x]),
+                   "rows": list(out["rows"][x])}
+            assert got == want, (sch, mode, [len(s) for s in t])
+
+
+def test_affine_long_triplets_vs_oracle(gpu_engine, oracle):
+    """Multi-block items (b, c beyond one 80-cell block, up to 4 x 4 blocks)."""
+    rng = np.random.default_rng(7)
+    trips = []
+    for lens in [(170, 20, 30), (5, 200, 180), (30, 165, 330), (190, 161, 159), (0, 170, 170), (240, 250, 260)]:
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in lens))
+    for mode in MODES:
+        sch = (1, -1, -2, -3)
+        out = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.affine(t, sch, mode)
+            assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
+
+
+def test_affine_c2_sample_vs_oracle(gpu_engine, oracle):
+    """Config C2 (150 bp, ~5% divergence): a prefix of the bench workload."""
+    seqs, offs = oracle.generate("fixed:150:150:150:24", 0.025, 0.005, 2)
+    sch = (1, -1, -2, -3)
+    out = ta.align_arrays(seqs, offs, ta.ScoringScheme(*sch), ta.AlignmentMode.Global)
+    rw = ta.align_arrays(seqs, offs, ta.ScoringScheme(*sch), ta.AlignmentMode.Global, with_rows=True,
+                         cell_budget=1 << 40)
+    for x in range(24):
+        t = tuple(bytes(seqs[offs[3 * x + d]:offs[3 * x + d + 1]]).decode() for d in range(3))
+        want = oracle.affine(t, sch, 0, with_rows=True)
+        assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], x
+        assert list(rw["rows"][x]) == want["rows"], x
+
+
+def test_affine_invalid_open_rejected(gpu_engine):
+    with pytest.raises(ta.InvalidArgument):
+        ta.ScoringScheme(1, -1, -2, 3).validate()
+    seqs, offs = trips_to_arrays([("ACGT", "ACGT", "ACGT")])
+    with pytest.raises(ta.InvalidArgument):
+        ta.align_arrays(seqs, offs, ta.ScoringScheme(1, -1, -2, 5), ta.AlignmentMode.Global)

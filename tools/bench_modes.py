@@ -20,19 +20,20 @@ def cells_of(offs):
     return int(np.prod(np.diff(offs).reshape(-1, 3).astype(np.int64), axis=1).sum())
 
 
-def score_run(name, spec, rates, seed, mode, reps=2, budget=1 << 40):
+def score_run(name, spec, rates, seed, mode, reps=2, budget=1 << 40, sch=SCH):
     seqs, offs = ta.generate(spec, *rates, seed)
     b = ta.DeviceBatch(seqs, offs)
     cfg = ta.EngineConfig(cell_budget=budget)
-    b.run(SCH, ta.AlignmentMode(mode), cfg)
+    b.run(sch, ta.AlignmentMode(mode), cfg)
     best = None
     for _ in range(reps):
-        b.run(SCH, ta.AlignmentMode(mode), cfg)
+        b.run(sch, ta.AlignmentMode(mode), cfg)
         st = b.stats()
         best = st["kernel_ms"] if best is None else min(best, st["kernel_ms"])
     out = b.fetch()
     c = cells_of(offs)
-    print(json.dumps({"case": name, "mode": ta.mode_name(ta.AlignmentMode(mode)), "triplets": len(offs) // 3,
+    print(json.dumps({"case": name, "mode": ta.mode_name(ta.AlignmentMode(mode)), "gap_open": sch.gap_open,
+                      "triplets": len(offs) // 3,
                       "cells": c, "kernel_ms": best, "gcups": c / best / 1e6, "lanes": st["lanes"],
                       "failed": int((out["status"] != 0).sum())}), flush=True)
 
@@ -49,7 +50,16 @@ def rows_run(name, spec, rates, seed, mode):
                       "failed": int((out["status"] != 0).sum())}), flush=True)
 
 
+AFF = ta.ScoringScheme(1, -1, -2, -3)
+
 if __name__ == "__main__":
+    import sys as _sys
+    if "--affine" in _sys.argv:
+        for mode in (0, 1, 2):
+            score_run("C2 prefix 100k affine", "fixed:150:150:150:100000", (0.025, 0.005), 2, mode, sch=AFF)
+        score_run("C3 prefix 20k affine", "fixed:250:250:250:20000", (0.025, 0.005), 3, 0, sch=AFF)
+        score_run("C4 prefix 5k affine", "uniform:64:512:5000", (0.08, 0.01), 4, 0, sch=AFF)
+        _sys.exit(0)
     for mode in (0, 1, 2):
         score_run("C2 prefix 200k", "fixed:150:150:150:200000", (0.025, 0.005), 2, mode)
     for mode in (0, 1, 2):
