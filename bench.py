@@ -12,9 +12,16 @@ named in BASELINE.json has no reference to be exact against.
   python bench.py --impl reference ...                    reference CPU path
 
 A step = one pass of the engine over this rank's shard of the batch.  With
-N GPUs (torchrun, one rank per GPU) each rank takes a contiguous 1/N slice
-(plan_partition "blocked", dispatch.cpp:37-41) -> strong scaling; there is no
-collective on the data path (barrier + max-reduce of timings only).
+N GPUs (torchrun, one rank per GPU) the workload is N x 1M triplets of the
+same generator stream and rank r takes the contiguous slice [r*1M, (r+1)*1M)
+(plan_partition "blocked", dispatch.cpp:37-41) -> weak scaling, per-GPU work
+fixed; there is no collective on the data path (barrier + max-reduce of
+timings only).
+
+  affine = the same C2 shape through the affine-gap kernels (SPEC-AFFINE.md,
+           gap_open -3; the reference has no affine gaps, so this is parity-
+           checked against the builder's oracle, not the reference), kernels
+           only on a 200k-triplet prefix of this rank's shard.
 
   value  = kernels only, inputs resident in HBM (DeviceBatch), CUDA events on
            the launching stream, L2 flushed (256 MiB write) between steps.
@@ -50,6 +57,7 @@ WORKLOAD = {
 OPS_PER_CELL = 13          # 7 add + 6 max per interior cell
 INT_LANES_PER_CLK_SM = 64  # measured: VIADDMNMX/VIMNMX3 issue rate (profiles/r01_intpeak.jsonl)
 SMS = 148
+AFFINE_OPEN = -3           # gap_open of the affine line (SPEC-AFFINE.md)
 
 
 def parse_args():
@@ -62,6 +70,8 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=2048, help="triplets timed on the host CPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-affine", action="store_true")
+    ap.add_argument("--affine-triplets", type=int, default=200000)
     return ap.parse_args()
 
 
@@ -191,7 +201,7 @@ def run_reference_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "GCUPS", "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic: reference generator, bit-identical inputs",
         "config": {"workload": f"{WORKLOAD['name']} {spec} rates {WORKLOAD['rates'][0]}:{WORKLOAD['rates'][1]} "
                                f"seed {WORKLOAD['seed']}, global, scheme 1/-1/-2 (linear gap); "
@@ -244,8 +254,12 @@ def main():
         return float(t.item())
 
     spec, n_total = workload_spec(args)
-    lo, hi = shard(n_total, rank, world)
-    seqs, offs = ta.generate(spec, *WORKLOAD["rates"], WORKLOAD["seed"], begin=lo, end=hi)
+    # weak scaling: N x n_total triplets of one generator stream, rank r takes the r-th block
+    parts = spec.split(":")
+    parts[-1] = str(n_total * world)
+    spec_all = ":".join(parts)
+    lo, hi = shard(n_total * world, rank, world)
+    seqs, offs = ta.generate(spec_all, *WORKLOAD["rates"], WORKLOAD["seed"], begin=lo, end=hi)
     n = (len(offs) - 1) // 3
     lens = np.diff(offs).reshape(-1, 3).astype(np.int64)
     cells = int(np.prod(lens, axis=1).sum())
@@ -316,6 +330,43 @@ def main():
                "host_input_bytes_per_step": int(seqs.nbytes + offs.nbytes),
                "ms_per_step": 1e3 * t_e2e / args.steps}
 
+    # ---- affine-gap kernels on the same shape (kernels only, prefix) --------
+    aff = None
+    if not args.no_affine:
+        m = min(n, args.affine_triplets)
+        a_off = offs[:3 * m + 1]
+        a_seq = seqs[:int(a_off[-1])]
+        a_cells = int(np.prod(np.diff(a_off).reshape(-1, 3).astype(np.int64), axis=1).sum())
+        asch = ta.ScoringScheme(*WORKLOAD["scheme"], gap_open=AFFINE_OPEN)
+        ab = ta.DeviceBatch(a_seq, a_off, device=local, stream=sh)
+        ab.run(asch, mode, stream=sh)
+        torch.cuda.synchronize()
+        barrier()
+        a_ms = []
+        for _ in range(max(1, args.steps - 1)):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            ab.run(asch, mode, stream=sh)
+            e1.record(stream)
+            e1.synchronize()
+            a_ms.append(e0.elapsed_time(e1))
+        ast = ab.stats()
+        a_out = ab.fetch(stream=sh)
+        t_aff = max_over_ranks(sum(a_ms) / 1e3)
+        a_val = sum_over_ranks(a_cells) * len(a_ms) / t_aff / 1e9
+        # affine roofline: 21 ALU-pipe instructions per cell-lane (affine.cuh)
+        f_a = 1965.0
+        alu_peak_gcups = SMS * INT_LANES_PER_CLK_SM * f_a * 1e6 / 21 * ast["lanes"] / 1e9
+        aff = {"value": a_val, "unit": "GCUPS", "gap_open": AFFINE_OPEN,
+               "workload": f"first {m} triplets of this rank's shard, global, scheme 1/-1/-2/open {AFFINE_OPEN}",
+               "triplets_per_s": sum_over_ranks(m) * len(a_ms) / t_aff, "lanes": ast["lanes"],
+               "failed_triplets": int((a_out["status"] != 0).sum()),
+               "alu_bound_gcups": alu_peak_gcups, "alu_frac": a_val / world / alu_peak_gcups,
+               "parity": "affine oracle (tests/test_gpu_affine.py); no reference affine exists"}
+        ab.close()
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -355,12 +406,13 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
+        "scaling": "weak", "vs_baseline": None,
         "dtype": "int16x2" if st["lanes"] == 2 else "int32",
         "data": "synthetic: reference generator (bit-identical), 2-bit packed in HBM",
         "config": {"workload": f"{WORKLOAD['name']} {spec} rates {WORKLOAD['rates'][0]}:{WORKLOAD['rates'][1]} "
                                f"seed {WORKLOAD['seed']}, global, scheme 1/-1/-2 (linear gap)",
-                   "triplets": n_total, "cells": int(cells_all), "parallelism": f"dp{world} (contiguous shards)",
+                   "triplets": n_total * world, "triplets_per_gpu": n_total, "cells": int(cells_all),
+                   "parallelism": f"dp{world} (contiguous shards, weak scaling)",
                    "l2": "flushed (256 MiB write) between timed steps"},
         "triplets_per_s": trip_s,
         "failed_triplets": bad,
@@ -369,6 +421,7 @@ def main():
         "e2e": e2e,
         "gpu_launches": int(st["launches"]) * args.steps,
         "clocks": clocks,
+        "affine": aff,
     }
     print(json.dumps(line), flush=True)
     if dist:

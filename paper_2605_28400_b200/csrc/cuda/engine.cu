@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -357,7 +358,8 @@ struct PinnedBuf {
 struct DeviceCtx {
   int device = -1;
   cudaStream_t stream = nullptr;
-  cudaStream_t copy = nullptr;  // H2D / D2H of the pipelined path
+  cudaStream_t copy = nullptr;  // H2D of the pipelined path
+  cudaStream_t d2h = nullptr;   // D2H of the pipelined path (never queues ahead of an H2D)
   int sms = 0;
   std::mutex mu;                // one pipelined call at a time per device
   // cached buffers of the pipelined score path (grow-only)
@@ -390,6 +392,7 @@ int get_ctx(int device, DeviceCtx** out) {
     TA_CK(cudaSetDevice(device));
     TA_CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     TA_CK(cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking));
+    TA_CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
     TA_CK(cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device));
     g_ctx[device] = std::move(ctx);
   }
@@ -1298,6 +1301,7 @@ void host_pack(const char* seqs, const int64_t* offs, int64_t lo, int64_t hi, co
 int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offsets, int64_t n,
                            const ta_scheme& scheme, const ta_options& opt, ta_results* out, cudaStream_t st) {
   std::lock_guard<std::mutex> lock(ctx->mu);
+  const auto tq0 = std::chrono::steady_clock::now();
   if (int rc = validate_scheme(scheme)) return rc;
   if (opt.mode < 0 || opt.mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "unknown alignment mode");
   const int cfg_rc = validate_options(opt);
@@ -1363,6 +1367,7 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     cut.push_back(n);
   }
   const int threads = int(std::max(1u, std::thread::hardware_concurrency()));
+  const bool prof = std::getenv("TA_PROFILE_PIPELINE") != nullptr;
   const int g2 = 2 * scheme.gap;
   ta::WaveArgs base{};
   base.seq = ctx->d_words.ptr;
@@ -1389,15 +1394,19 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   std::vector<std::unique_ptr<BucketLaunch>> keep;  // plans stay alive until the end (no cudaFree mid-pipeline)
   int64_t launches = 0;
   int rc = TA_OK;
+  const auto tq1 = std::chrono::steady_clock::now();
   for (size_t k = 0; k + 1 < cut.size() && rc == TA_OK; ++k) {
     const int64_t lo = cut[k], hi = cut[k + 1];
     if (hi <= lo) continue;
     const uint32_t w0 = wofs[3 * size_t(lo)];
     const uint32_t w1 = hi < n ? wofs[3 * size_t(hi)] : uint32_t(words);
     PinnedBuf<uint32_t>& slot = ctx->h_words[k & 1];
+    const auto tp0 = std::chrono::steady_clock::now();
     TA_CK(cudaEventSynchronize(slot_free[k & 1]));  // the previous H2D from this slot is done
     TA_CK(slot.reserve(size_t(w1 - w0) + 2));
+    const auto tp1 = std::chrono::steady_clock::now();
     host_pack(seqs, offsets, lo, hi, wofs, w0, slot.ptr, status, threads);
+    const auto tp2 = std::chrono::steady_clock::now();
     TA_CK(cudaMemcpyAsync(ctx->d_words.ptr + w0, slot.ptr, size_t(w1 - w0) * 4, cudaMemcpyHostToDevice, ctx->copy));
     TA_CK(cudaEventRecord(slot_free[k & 1], ctx->copy));
     std::vector<std::vector<int32_t>> buckets(ta::kNumGrid);
@@ -1452,14 +1461,23 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
       TA_CK(cudaGetLastError());
     }
     TA_CK(cudaEventRecord(kdone, st));
-    TA_CK(cudaStreamWaitEvent(ctx->copy, kdone, 0));
+    TA_CK(cudaStreamWaitEvent(ctx->d2h, kdone, 0));
+    if (prof) {
+      const auto tp3 = std::chrono::steady_clock::now();
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[ta pipeline] chunk %zu: wait %.2f ms  pack %.2f ms  plan+launch %.2f ms\n", k,
+                   ms(tp0, tp1), ms(tp1, tp2), ms(tp2, tp3));
+    }
     TA_CK(cudaMemcpyAsync(ctx->h_out.ptr + lo, ctx->d_score.ptr + lo, size_t(hi - lo) * 4, cudaMemcpyDeviceToHost,
-                          ctx->copy));
+                          ctx->d2h));
     TA_CK(cudaMemcpyAsync(ctx->h_out.ptr + nn + 3 * size_t(lo), ctx->d_end.ptr + 3 * lo, size_t(hi - lo) * 12,
-                          cudaMemcpyDeviceToHost, ctx->copy));
+                          cudaMemcpyDeviceToHost, ctx->d2h));
   }
-  const cudaError_t e1 = cudaStreamSynchronize(ctx->copy);
+  const auto tq2 = std::chrono::steady_clock::now();
+  cudaError_t e1 = cudaStreamSynchronize(ctx->copy);
+  if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(ctx->d2h);
   const cudaError_t e2 = cudaStreamSynchronize(st);
+  const auto tq3 = std::chrono::steady_clock::now();
   for (auto& e : slot_free) cudaEventDestroy(e);
   cudaEventDestroy(h2d_done);
   cudaEventDestroy(kdone);
@@ -1472,6 +1490,11 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     if (out->ends)
       for (int d = 0; d < 3; ++d) out->ends[3 * t + d] = ok ? ctx->h_out.ptr[nn + 3 * t + d] : 0;
     if (out->status) out->status[t] = status[t];
+  }
+  if (prof) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "[ta pipeline] prologue %.2f ms  chunks %.2f ms  drain %.2f ms  epilogue %.2f ms\n",
+                 ms(tq0, tq1), ms(tq1, tq2), ms(tq2, tq3), ms(tq3, std::chrono::steady_clock::now()));
   }
   if (cfg_rc) g_err = cfg_msg;
   return TA_OK;
