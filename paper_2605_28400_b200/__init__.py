@@ -135,10 +135,11 @@ def lib() -> ctypes.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("TA_LIB_PATH_EXPERIMENT", LIB_PATH)  # dev-only: A/B a variant build of the same ABI
+    if not os.path.exists(path):
         raise ImportError(f"{LIB_PATH} is missing: build it with `make -C {HERE}` "
                           "(the B200 engine has no CPU fallback)")
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     vp, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.ta_last_error.restype = ctypes.c_char_p
     L.ta_version.restype = ctypes.c_char_p

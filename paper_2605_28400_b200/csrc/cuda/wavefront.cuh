@@ -376,17 +376,20 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       }
       const int sc = TRACE ? 16 : 1;
       const int tg = TRACE ? static_cast<int>(kTagT4) : 0;
+      // sigma12' in the sweep's anti-diagonal cell order, 4 cells per STS.128
+      uint32_t v[4];
+      int k = 0;
 #pragma unroll
-      for (int g = 0; g < NN / 4; ++g) {
-        uint32_t v[4];
+      for (int d = 0; d <= 2 * N - 2; ++d)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int cell = g * 4 + e, p = cell / N, q = cell % N;
+        for (int p = 0; p < N; ++p) {
+          const int q = d - p;
+          if (q < 0 || q >= N) continue;
           const int sv = ((ld.v1 >> p) & (ld.v2 >> q) & 1u) ? ((((c1 >> (2 * p)) & 3u) == ((c2 >> (2 * q)) & 3u)) ? mp : mm) : 0;
-          v[e] = static_cast<uint32_t>(sv * sc + tg);
+          v[k & 3] = static_cast<uint32_t>(sv * sc + tg);
+          if ((k & 3) == 3) s12v[(k >> 2) * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
+          ++k;
         }
-        s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
-      }
     } else {
       // byte tables: sigma'(code, x) = mm + (mp - mm) * [code == x], byte `code`
       const uint32_t mm8 = static_cast<uint32_t>(mm) * 0x01010101u;
@@ -400,17 +403,19 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         reinterpret_cast<uint32_t*>(tab2)[(p * T + t) * 2 + l] = t2w[p];
       }
       uint16_t* s12h = reinterpret_cast<uint16_t*>(s12w);
+      int k = 0;
 #pragma unroll
-      for (int p = 0; p < N; ++p) {
-        const uint32_t x1 = (c1 >> (2 * p)) & 3u;
-        const uint32_t sel = x1 | ((x1 | 8u) << 4);
+      for (int d = 0; d <= 2 * N - 2; ++d)
 #pragma unroll
-        for (int q = 0; q < N; ++q) {
-          const int cell = p * N + q;
-          s12h[((size_t(cell >> 2) * T + t) * 4 + (cell & 3)) * 2 + l] =
+        for (int p = 0; p < N; ++p) {
+          const int q = d - p;
+          if (q < 0 || q >= N) continue;
+          const uint32_t x1 = (c1 >> (2 * p)) & 3u;
+          const uint32_t sel = x1 | ((x1 | 8u) << 4);
+          s12h[((size_t(k >> 2) * T + t) * 4 + (k & 3)) * 2 + l] =
               ((ld.v1 >> p) & 1u) ? static_cast<uint16_t>(prmt(t2w[q], 0u, sel)) : uint16_t(0);
+          ++k;
         }
-      }
     }
   };
 
@@ -437,16 +442,18 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       sel[p] = x10 | ((x10 | 8u) << 4) | (x11 << 8) | ((x11 | 8u) << 12);
       pm[p] = (((l0.v1 >> p) & 1u) ? 0x0000FFFFu : 0u) | (((l1.v1 >> p) & 1u) ? 0xFFFF0000u : 0u);
     }
+    uint32_t v[4];
+    int k = 0;
 #pragma unroll
-    for (int g = 0; g < NN / 4; ++g) {
-      uint32_t v[4];
+    for (int d = 0; d <= 2 * N - 2; ++d)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int cell = g * 4 + e, p = cell / N, q = cell % N;
-        v[e] = prmt(t2a[q], t2b[q], sel[p]) & pm[p];
+      for (int p = 0; p < N; ++p) {
+        const int q = d - p;
+        if (q < 0 || q >= N) continue;
+        v[k & 3] = prmt(t2a[q], t2b[q], sel[p]) & pm[p];
+        if ((k & 3) == 3) s12v[(k >> 2) * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
+        ++k;
       }
-      s12v[g * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
-    }
   };
 
   auto setup = [&](int l, int it, int iend) { tables_lane(l, fetch(l, it, iend)); };
@@ -638,20 +645,34 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       // instance of the tile loop, so ordinary steps carry no forcing maxima.
       auto sweep_tile = [&](auto force_tag) {
       constexpr bool FORCE = decltype(force_tag)::value;
-      uint4 sg4 = make_uint4(0, 0, 0, 0);
+      // Cells in anti-diagonal order (d = P + Q): consecutive cells are
+      // independent, so the row / column dependencies of the recurrence are
+      // ~N instructions apart instead of back to back.  sigma12' is stored in
+      // the same order (4 cells per LDS.128).
+      uint32_t a1v[N];
 #pragma unroll
-      for (int P = 1; P <= N; ++P) {
-        uint32_t a1 = sig_row(tab1, P - 1);
-        if constexpr (TRACE) a1 = a1 * 16u + kTagT2;
-        [[maybe_unused]] uint32_t fl = flrow;
+      for (int p = 0; p < N; ++p) {
+        a1v[p] = sig_row(tab1, p);
+        if constexpr (TRACE) a1v[p] = a1v[p] * 16u + kTagT2;
+      }
+      uint4 sg4 = make_uint4(0, 0, 0, 0);
+      [[maybe_unused]] uint32_t fd = flrow;  // local floor of diagonal d (depends on P + Q only)
+      int k = 0;
+#pragma unroll
+      for (int d = 0; d <= 2 * N - 2; ++d) {
         if constexpr (MODE == kLocal) {
-          if (P < N) flrow = fma_add(flrow, one, ag2s);
+          if (d > 0) fd = fma_add(fd, one, ag2s);
         }
 #pragma unroll
-        for (int Q = 1; Q <= N; ++Q) {
+        for (int P0 = 0; P0 < N; ++P0) {
+          const int Q0 = d - P0;
+          if (Q0 < 0 || Q0 >= N) continue;
+          const int P = P0 + 1, Q = Q0 + 1;
           const int cell = (P - 1) * N + (Q - 1);
-          if ((cell & 3) == 0) sg4 = s12v[(cell >> 2) * T + t];
-          const uint32_t sg = (cell & 3) == 0 ? sg4.x : (cell & 3) == 1 ? sg4.y : (cell & 3) == 2 ? sg4.z : sg4.w;
+          if ((k & 3) == 0) sg4 = s12v[(k >> 2) * T + t];
+          const uint32_t sg = (k & 3) == 0 ? sg4.x : (k & 3) == 1 ? sg4.y : (k & 3) == 2 ? sg4.z : sg4.w;
+          ++k;
+          const uint32_t a1 = a1v[P - 1];
           const uint32_t a2 = s02[Q - 1];
           uint32_t x;
           if constexpr (!TRACE) {
@@ -671,10 +692,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::addmax(Pv[P][Q], kTagT5, x);                    // t5
             x = Ops::addmax(Cu[P - 1][Q], kTagT6, x);                // t6
           }
-          if constexpr (MODE == kLocal) {
-            x = Ops::addmax(fl, one ^ 1u, x);  // floor 0 (oracle.cpp:59); fused form, no s16x2 re-pack
-            if (Q < N) fl = fma_add(fl, one, ag2s);
-          }
+          if constexpr (MODE == kLocal) x = Ops::addmax(fd, one ^ 1u, x);  // floor 0 (oracle.cpp:59), fused form
           if constexpr (MODE == kGlobal || MODE == kSemi) {
             if (P == 1 && Q == 1) x = Ops::max2(x, fcorner);
           }
