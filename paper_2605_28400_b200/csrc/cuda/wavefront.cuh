@@ -30,6 +30,10 @@
 #include <cstdint>
 #include <type_traits>
 
+#ifndef TA_MBAR_SUSPEND_NS
+#define TA_MBAR_SUSPEND_NS 0
+#endif
+
 namespace ta {
 
 constexpr int kGlobal = 0;
@@ -164,10 +168,19 @@ __device__ __forceinline__ void mbar_arrive_group(uint64_t* bar) {
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+#if TA_MBAR_SUSPEND_NS > 0
+  // suspend (up to the hint) instead of spinning: a waiting warp does not
+  // steal issue slots from the warps still computing the step
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1, %2;\n @!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity), "n"(TA_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(a),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __device__ __forceinline__ uint32_t lop_sel(uint32_t a, uint32_t b, uint32_t m) {

@@ -17,6 +17,14 @@ for mode in (0, 2):
         best = min(best, b.stats()["kernel_ms"])
     cells = 674981204837
     print(json.dumps({"lib": os.environ.get("TA_LIB_PATH_EXPERIMENT", "in-tree"), "mode": mode, "gcups": cells / best / 1e6}))
+AFF = ta.ScoringScheme(1, -1, -2, -3)
+sa, oa = ta.generate("fixed:150:150:150:50000", 0.025, 0.005, 2)
+ba = ta.DeviceBatch(sa, oa)
+best = 1e9
+for _ in range(3):
+    ba.run(AFF, ta.AlignmentMode(0), ta.EngineConfig(cell_budget=1 << 40))
+    best = min(best, ba.stats()["kernel_ms"])
+print(json.dumps({"lib": os.environ.get("TA_LIB_PATH_EXPERIMENT", "in-tree"), "mode": "affine-global", "gcups": ba.stats()["cells"] / best / 1e6}))
 PY
 python /tmp/ab.py
 TA_LIB_PATH_EXPERIMENT="$1" python /tmp/ab.py
