@@ -66,6 +66,12 @@ struct DevBuf {
   }
 };
 
+struct WaveRound {
+  int ctas = 0;
+  int soff_at = 0;   // this round's stream offsets start at soff[soff_at]
+  int steps_at = 0;  // and its per-CTA step counts at steps[steps_at]
+};
+
 struct BucketLaunch {
   int grid = 0, lanes = 0, mode = 0;
   bool wave = false;
@@ -76,6 +82,7 @@ struct BucketLaunch {
   DevBuf<int32_t> faces;
   DevBuf<int64_t> face_off;
   DevBuf<int64_t> wave_base;  // wave mode: per triplet id, face area in 8-byte entries
+  std::vector<WaveRound> rounds;  // wave mode: launches in dependency order
   int64_t face_bytes = 0;
   uint32_t epoch = 0;         // wave mode: tag epoch of the last launch
   int64_t padded = 0;
@@ -636,6 +643,7 @@ void plan_streams(const std::vector<int32_t>& ids, const std::vector<int32_t>& a
 struct WavePlan {
   std::vector<int4> items;
   std::vector<int32_t> soff, steps;
+  std::vector<WaveRound> rounds;
   std::vector<int64_t> base;  // per triplet id (only wave triplets set)
   int64_t entries = 0;
   int64_t padded_slices = 0;
@@ -678,29 +686,38 @@ void plan_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, c
     pairs.push_back({x, make_int4(-1, 0, x.z, 0x00010001)});
     i += 1;
   }
-  const int C = int(std::max<size_t>(1, std::min<size_t>(size_t(max_ctas), pairs.size())));
-  *ctas_out = C;
-  std::vector<std::vector<int4>> lists(size_t(C) * lanes);
-  std::vector<int64_t> load(size_t(C), 0);
-  for (size_t k = 0; k < pairs.size(); ++k) {
-    const size_t cta = k % size_t(C);
-    lists[cta * lanes].push_back(pairs[k].first);
-    if (lanes == 2) lists[cta * 2 + 1].push_back(pairs[k].second);
-    load[cta] += pairs[k].first.z;
-  }
+  // One pair per CTA and launch: a CTA that held two wave items would start
+  // the second (its front tiles) while its back tiles still finish the first,
+  // and a wait in the second could then block producers others wait on.  So
+  // pairs beyond the resident CTA count go to a later launch (round); faces
+  // of earlier rounds are complete and tagged when a round starts.
+  const size_t C = size_t(std::max(1, max_ctas));
   out->items.clear();
-  out->soff.assign(size_t(C) * lanes + 1, 0);
-  out->steps.assign(size_t(C), 0);
+  out->soff.clear();
+  out->steps.clear();
+  out->rounds.clear();
   out->padded_slices = 0;
-  for (size_t st = 0; st < lists.size(); ++st) {
-    out->soff[st] = int32_t(out->items.size());
-    for (const int4& it : lists[st]) {
-      out->items.push_back(it);
-      if (it.x >= 0) out->padded_slices += it.z;
+  for (size_t k0 = 0; k0 < pairs.size(); k0 += C) {
+    const size_t k1 = std::min(pairs.size(), k0 + C);
+    WaveRound rd;
+    rd.ctas = int(k1 - k0);
+    rd.soff_at = int(out->soff.size());
+    rd.steps_at = int(out->steps.size());
+    for (size_t k = k0; k < k1; ++k) {
+      out->soff.push_back(int32_t(out->items.size()));
+      out->items.push_back(pairs[k].first);
+      if (lanes == 2) {
+        out->soff.push_back(int32_t(out->items.size()));
+        out->items.push_back(pairs[k].second);
+      }
+      if (pairs[k].first.x >= 0) out->padded_slices += pairs[k].first.z;
+      if (lanes == 2 && pairs[k].second.x >= 0) out->padded_slices += pairs[k].second.z;
+      out->steps.push_back(int32_t(pairs[k].first.z + 2 * (grid - 1)));
     }
+    out->soff.push_back(int32_t(out->items.size()));
+    out->rounds.push_back(rd);
   }
-  out->soff[lists.size()] = int32_t(out->items.size());
-  for (int cta = 0; cta < C; ++cta) out->steps[size_t(cta)] = int32_t(load[size_t(cta)] + 2 * (grid - 1));
+  *ctas_out = out->rounds.empty() ? 0 : out->rounds[0].ctas;
 }
 
 // Long triplets go to wave mode when there are too few of them to fill the
@@ -745,6 +762,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
     int ctas = 0;
     plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, grid, int64_t(bt->a.size()), &plan, &ctas);
     bl->ctas = ctas;
+    bl->rounds = plan.rounds;
     TA_CK(bl->items.reserve(plan.items.size()));
     TA_CK(bl->soff.reserve(plan.soff.size()));
     TA_CK(bl->steps.reserve(plan.steps.size()));
@@ -808,6 +826,15 @@ int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st,
     }
     args.wave_base = bl->wave_base.ptr;
     args.epoch = bl->epoch;
+    for (const WaveRound& rd : bl->rounds) {
+      ta::WaveArgs ra = args;
+      ra.stream_off = bl->soff.ptr + rd.soff_at;
+      ra.cta_steps = bl->steps.ptr + rd.steps_at;
+      bl->ke.fn<<<rd.ctas, bl->ke.threads, bl->ke.smem, st>>>(ra);
+      TA_CK(cudaGetLastError());
+      *launches += 1;
+    }
+    return TA_OK;
   }
   bl->ke.fn<<<bl->ctas, bl->ke.threads, bl->ke.smem, st>>>(args);
   TA_CK(cudaGetLastError());

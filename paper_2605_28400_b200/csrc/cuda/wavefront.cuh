@@ -513,7 +513,22 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     // Every thread (active or idle) waits for the previous phase before it
     // arrives again: no thread can arrive on mbar[b] twice within one phase.
     if (s > 0) mbar_wait(&mbar[buf ^ 1], static_cast<uint32_t>((s - 1) >> 1) & 1u);
+    // A tile that holds no real cell of any live lane this step (padding
+    // beyond b / c, or the padded slices of a block item) skips the sweep: its
+    // values only ever feed other padding, and its warp's issue slots go to
+    // the tiles doing real work.
+    // (Measured per mode: +64% for local, -4..7% for the others, whose
+    // register allocation it perturbs; so only local mode skips.)
+    constexpr bool kSkipPadding = MODE == kLocal;
+    bool work = !kSkipPadding;
+    if constexpr (kSkipPadding) {
+#pragma unroll
+      for (int l = 0; l < LANES; ++l)
+        work |= !(flags[l] & kDone) && si[l] <= la[l] && LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 &&
+                LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
+    }
     if (active) {
+     if (work) {
       constexpr int NW = (NN + 7) / 8;
       uint32_t Cu[N + 1][N + 1];
       uint32_t dirw[TRACE ? NW : 1];
@@ -548,12 +563,15 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
                 }
                 return static_cast<int32_t>(v.x);
               };
-              if (r == 0 && (flags[l] & kInTop) && ok) {
+              // only a lane for which this tile holds real cells waits for its
+              // faces: padding producers of the other lane skip their sweep
+              const bool real = LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 && LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
+              if (r == 0 && (flags[l] & kInTop) && ok && real) {
                 const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kSegE;
 #pragma unroll
                 for (int q = 0; q <= N; ++q) Cu[0][q] = lop_sel(Cu[0][q], Ops::splat(take(cc, src, q) << SH), Ops::mask(l));
               }
-              if (cc == 0 && (flags[l] & kInLeft) && ok) {
+              if (cc == 0 && (flags[l] & kInLeft) && ok && real) {
                 const uint64_t* src = fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE;
 #pragma unroll
                 for (int p = 0; p < N; ++p)
@@ -955,6 +973,10 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       for (int P = 0; P <= N; ++P)
 #pragma unroll
         for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = Cu[P][Q];
+
+     } else {
+      mbar_arrive_group(&mbar[buf]);
+     }
 
       // ---- 9. advance the lanes (switch triplets at the end of a stream item)
       bool sw[LANES];
