@@ -123,3 +123,29 @@ def test_affine_invalid_open_rejected(gpu_engine):
     seqs, offs = trips_to_arrays([("ACGT", "ACGT", "ACGT")])
     with pytest.raises(ta.InvalidArgument):
         ta.align_arrays(seqs, offs, ta.ScoringScheme(1, -1, -2, 5), ta.AlignmentMode.Global)
+
+
+def test_cli_gap_open_matches_oracle(gpu_engine, oracle, tmp_path):
+    """`trioalign align --gap-open` (the one added CLI flag) writes the
+    affine scores of SPEC-AFFINE.md in the reference CSV format."""
+    import os
+    import subprocess
+    rng = np.random.default_rng(21)
+    trips = rand_trips(rng, 6, 5, 40)
+    fa = tmp_path / "in.fa"
+    with open(fa, "w") as f:
+        for x, t in enumerate(trips):
+            for d, s in enumerate(t):
+                f.write(f">t{x}_{d}\n{s}\n")
+    exe = os.path.join(os.path.dirname(ta.__file__), "trioalign")
+    for mode, name in ((0, "global"), (1, "semiglobal"), (2, "local")):
+        out = tmp_path / f"o{mode}.csv"
+        p = subprocess.run([exe, "align", "--in", str(fa), "--out", str(out), "--mode", name, "--gap-open", "-3"],
+                           capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+        lines = out.read_text().strip().splitlines()
+        assert lines[0] == "id,mode,score,i,j,k,error"
+        for x, line in enumerate(lines[1:]):
+            f = line.split(",")
+            want = oracle.affine(trips[x], (1, -1, -2, -3), mode)
+            assert f[1] == name and int(f[2]) == want["score"] and [int(v) for v in f[3:6]] == want["end"], line

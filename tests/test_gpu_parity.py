@@ -210,3 +210,19 @@ def test_c5_single_long_triplets_vs_reference(gpu_engine, oracle):
         assert int(out["status"][0]) == 0, name
         assert int(out["score"][0]) == want["score"], name
         assert list(out["end"][0]) == want["end"], name
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_wave_pairs_of_different_triplets(gpu_engine, oracle, mode):
+    """Wave mode (few long triplets spread over all CTAs) pairing blocks of
+    DIFFERENT triplets with equal a but different b, c in the two lanes: a
+    tile can be padding for one lane and real for the other."""
+    rng = np.random.default_rng(55 + mode)
+    trips = []
+    for b, c in [(165, 300), (310, 170), (200, 200), (330, 161), (161, 330), (250, 180)]:
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (180, b, c)))
+    out = run(trips, (1, -1, -2), mode)
+    for x, t in enumerate(trips):
+        want = oracle.align(t, (1, -1, -2), mode)
+        assert int(out["status"][x]) == 0
+        assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)

@@ -101,6 +101,18 @@ def test_scheme_validation():
     assert ta.lib().ta_validate_scheme(ctypes.byref(ta._Scheme(1, -1, -2))) == 0
 
 
+def test_affine_scheme_validation():  # SPEC-AFFINE.md: gap_open <= 0, |gap_open| <= 1024
+    for bad in [(1, -1, -2, 1), (1, -1, -2, -1025)]:
+        with pytest.raises(ta.InvalidArgument):
+            ta.ScoringScheme(*bad).validate()
+        assert ta.lib().ta_validate_scheme(ctypes.byref(ta._Scheme(*bad))) == 7
+    ta.ScoringScheme(1, -1, -2, -3).validate()
+    assert ta.lib().ta_validate_scheme(ctypes.byref(ta._Scheme(1, -1, -2, -3))) == 0
+    # the C-ABI structs match the header (4 x int32 scheme; options end with gap_model)
+    assert ctypes.sizeof(ta._Scheme) == 16
+    assert [f for f, _ in ta._Options._fields_][-1] == "gap_model"
+
+
 def test_engine_config_validation():
     with pytest.raises(ta.ConfigError):
         ta.EngineConfig(tile_size=0).validate()

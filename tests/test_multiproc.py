@@ -87,3 +87,19 @@ def test_generator_slices_concatenate_to_the_full_dataset():
     parts = [ta.generate(SPEC, *RATES, SEED, begin=lo, end=hi) for lo, hi in ((0, 10), (10, 11), (11, 37))]
     cat = b"".join(p[0][:int(p[1][-1])].tobytes() for p in parts)
     assert cat == seqs[:int(offs[-1])].tobytes()
+
+
+def test_weak_scaling_shards_extend_the_single_gpu_workload():
+    """bench.py at N GPUs: N x n triplets of one generator stream, rank r the
+    r-th block of n; rank 0's shard is exactly the 1-GPU workload."""
+    import bench
+    import paper_2605_28400_b200 as ta
+    n, world = 12, 3
+    one, one_off = ta.generate(f"fixed:20:20:20:{n}", 0.05, 0.01, 2)
+    for rank in range(world):
+        lo, hi = bench.shard(n * world, rank, world)
+        assert (lo, hi) == (rank * n, (rank + 1) * n)
+        seqs, offs = ta.generate(f"fixed:20:20:20:{n * world}", 0.05, 0.01, 2, begin=lo, end=hi)
+        assert len(offs) == 3 * n + 1
+        if rank == 0:
+            assert seqs[:int(offs[-1])].tobytes() == one[:int(one_off[-1])].tobytes()
