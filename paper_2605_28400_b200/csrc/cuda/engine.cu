@@ -377,6 +377,7 @@ struct DeviceCtx {
   DevBuf<ta::TripletDesc> d_desc;
   DevBuf<int32_t> d_score, d_end;
   DevBuf<unsigned long long> d_key;
+  std::vector<std::unique_ptr<BucketLaunch>> plan_pool;  // pipelined path launch plans (grow-only)
 };
 
 std::mutex g_ctx_mu;
@@ -1380,13 +1381,24 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   // chunks: contiguous triplet ranges of ~equal cells
   int64_t total_cells = 0;
   for (size_t t = 0; t < nn; ++t) total_cells += int64_t(a[t]) * b[t] * c[t];
+  // Chunk boundaries by cells: the first chunks are small (1/64, 1/64, 1/32,
+  // 1/16 of the batch) so the GPU starts early; the rest are equal.
   const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(16, n / 20000));
+  std::vector<double> frac;  // cumulative cell fractions at the cuts
+  if (nchunks >= 8) {
+    double at = 0;
+    for (double f : {1.0 / 64, 1.0 / 64, 1.0 / 32, 1.0 / 16}) frac.push_back(at += f);
+    for (int64_t k = 1; k < nchunks - 1; ++k) frac.push_back(at + (1.0 - at) * double(k) / double(nchunks - 1));
+  } else {
+    for (int64_t k = 1; k < nchunks; ++k) frac.push_back(double(k) / double(nchunks));
+  }
   std::vector<int64_t> cut{0};
   {
-    int64_t acc = 0, k = 1;
+    int64_t acc = 0;
+    size_t k = 0;
     for (int64_t t = 0; t < n; ++t) {
       acc += int64_t(a[size_t(t)]) * b[size_t(t)] * c[size_t(t)];
-      if (k < nchunks && acc * nchunks >= total_cells * k && t + 1 < n) {
+      if (k < frac.size() && double(acc) >= frac[k] * double(total_cells) && t + 1 < n) {
         cut.push_back(t + 1);
         ++k;
       }
@@ -1418,7 +1430,17 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   shim.a.swap(a);
   shim.b.swap(b);
   shim.c.swap(c);
-  std::vector<std::unique_ptr<BucketLaunch>> keep;  // plans stay alive until the end (no cudaFree mid-pipeline)
+  // Launch plans come from a per-device pool that outlives the call: no
+  // cudaMalloc / cudaFree (which can stall the host or the device) inside the
+  // pipeline, and repeated calls reuse the buffers.
+  size_t pool_used = 0;
+  auto take_plan = [&]() -> BucketLaunch* {
+    if (pool_used == ctx->plan_pool.size()) ctx->plan_pool.push_back(std::make_unique<BucketLaunch>());
+    BucketLaunch* bl = ctx->plan_pool[pool_used++].get();
+    bl->wave = false;
+    bl->rounds.clear();
+    return bl;
+  };
   int64_t launches = 0;
   int rc = TA_OK;
   const auto tq1 = std::chrono::steady_clock::now();
@@ -1459,17 +1481,15 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
       for (int w = 0; w < 2 && rc == TA_OK; ++w) {
         const std::vector<int32_t>& part = w ? wave_ids : rest_ids;
         if (part.empty()) continue;
-        keep.push_back(std::make_unique<BucketLaunch>());
-        rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy, keep.back().get(),
-                            w == 1);
-        launch_now.push_back(keep.back().get());
+        BucketLaunch* bl = take_plan();
+        rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy, bl, w == 1);
+        launch_now.push_back(bl);
       }
     }
     if (rc != TA_OK) break;
     DevBuf<int32_t>* ids_buf = nullptr;
     if (opt.mode != TA_GLOBAL && !ok_ids.empty()) {
-      keep.push_back(std::make_unique<BucketLaunch>());
-      ids_buf = &keep.back()->soff;
+      ids_buf = &take_plan()->soff;
       TA_CK(ids_buf->reserve(ok_ids.size()));
       TA_CK(cudaMemcpyAsync(ids_buf->ptr, ok_ids.data(), ok_ids.size() * 4, cudaMemcpyHostToDevice, ctx->copy));
       TA_CK(cudaMemsetAsync(ctx->d_key.ptr + lo, 0, size_t(hi - lo) * 8, ctx->copy));
