@@ -20,8 +20,8 @@
 // (primes: previous slice).  A thread keeps B, E2, E3, E5 of its tile for the
 // next slice and E4, E6, E7 for the cells to its right / below; the mailbox
 // carries (B, E3, E4, E7) of the right column and (B, E4, E2, E6) of the bottom
-// row.  21 ALU-pipe (VIADDMNMX / VIMNMX3) + 5 FMA-pipe (IMAD) instructions
-// per cell; values are gap-shifted (-2 gap (i+j+k)) and biased by -8 open so
+// row.  16 ALU-pipe (VIADDMNMX / VIMNMX3) + 10 FMA-pipe (IMAD) instructions
+// per cell; values are gap-shifted (-2 gap (i+j+k)) and biased by -10 open so
 // that every real value is >= 0 and packed s16x2 adds on the FMA pipe are
 // exact.  TRACE: values carry a 3-bit type tag (7 - t) in their low bits, the
 // maxima select the smallest type on ties (SPEC-AFFINE.md traceback rule), and
@@ -126,7 +126,13 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   const int ag2 = -g2;
   const uint32_t one = args.one;
   const uint32_t op1 = Ops::splat(args.open * SC);      // + open   (lane-safe ALU adds)
-  const uint32_t op2 = Ops::splat(2 * args.open * SC);  // + 2 open
+  // + open / + 2 open as plain 32-bit adds on the FMA pipe: the bias (-10 open)
+  // keeps every real V >= 2 |open| and B >= 4 |open|, so subtracting never
+  // borrows across the s16x2 lanes (NEG = -16384 per lane stays negative).
+  const uint32_t osub1 = LANES == 2 ? 0u - static_cast<uint32_t>(-args.open * SC) * 0x00010001u
+                                    : static_cast<uint32_t>(args.open * SC);
+  const uint32_t osub2 = LANES == 2 ? 0u - static_cast<uint32_t>(-2 * args.open * SC) * 0x00010001u
+                                    : static_cast<uint32_t>(2 * args.open * SC);
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
   for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
@@ -456,9 +462,9 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               v7 = v7 & ~7u;
             }
             const uint32_t b = Ops::max3(Ops::max3(Ops::max3(v1, v2, v3), v4, v5), v6, v7);
-            const uint32_t b2 = Ops::addmax(b, op2, NEG);
-            const uint32_t w2 = Ops::addmax(v2, op1, NEG), w3 = Ops::addmax(v3, op1, NEG);
-            const uint32_t w5 = Ops::addmax(v5, op1, NEG), w6 = Ops::addmax(v6, op1, NEG);
+            const uint32_t b2 = fma_add(b, one, osub2);
+            const uint32_t w2 = fma_add(v2, one, osub1), w3 = fma_add(v3, one, osub1);
+            const uint32_t w5 = fma_add(v5, one, osub1), w6 = fma_add(v6, one, osub1);
             cB[P][Q] = b;
             cE2[P][Q] = Ops::addmax(v6, op1, Ops::max3(v2, w5, b2));
             cE3[P][Q] = Ops::addmax(v7, op1, Ops::max3(v3, w5, b2));

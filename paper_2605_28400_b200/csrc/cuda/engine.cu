@@ -864,7 +864,7 @@ int64_t aff_lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c) {
   const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
   const int warps = (ta::kAffG * ta::kAffG + 31) / 32;
   const int64_t slices = std::max<int64_t>(a + 1, ta::kAffG + 2 + warps);
-  return -8 * int64_t(s.gap_open) + int64_t(s.match - g2) * (slices + ej + ek);
+  return -10 * int64_t(s.gap_open) + int64_t(s.match - g2) * (slices + ej + ek);
 }
 
 bool aff_s16_ok(const ta_scheme& s, int64_t max_bound) {
@@ -938,7 +938,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
   base.match_p = scheme.match - base.g2;
   base.mismatch_p = scheme.mismatch - base.g2;
   base.open = scheme.gap_open;
-  base.bias = -8 * scheme.gap_open;
+  base.bias = -10 * scheme.gap_open;
   base.one = 1u;
   if (!bt->ev0) TA_CK(cudaEventCreate(&bt->ev0));
   if (!bt->ev1) TA_CK(cudaEventCreate(&bt->ev1));
