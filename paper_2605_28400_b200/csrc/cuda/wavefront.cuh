@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           for (int l = 0; l < LANES; ++l) {
             const bool ok = si[l] <= la[l];
             if constexpr (WAVE) {
+              if (LS(l, kTid) < 0) continue;  // a null item (idle partner lane) has no faces
               const uint32_t want = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
               const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
               const int a1 = la[l] + 1;
@@ -1046,6 +1047,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         if ((flags[l] & kDone) || si[l] > la[l]) continue;
         const int a1 = la[l] + 1;
         if constexpr (WAVE) {
+          if (LS(l, kTid) < 0 || !(flags[l] & (kInTop | kInLeft))) continue;
           const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
           const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
           auto fetch_seg = [&](int seg, const uint64_t* src) {
