@@ -794,7 +794,14 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
   int per_sm = 0;
   TA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ke.fn, ke.threads, ke.smem));
-  if (per_sm < 1) return fail(TA_ERR_CUDA, "wavefront kernel does not fit on an SM");
+  if (per_sm < 1) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, ke.fn);
+    return fail(TA_ERR_CUDA, "wavefront kernel does not fit on an SM (grid " + std::to_string(grid) + ", " +
+                                 std::to_string(ke.threads) + " threads, " + std::to_string(fa.numRegs) + " regs, " +
+                                 std::to_string(ke.smem) + " B dynamic smem, max threads " +
+                                 std::to_string(fa.maxThreadsPerBlock) + ")");
+  }
   const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
   bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
   StreamPlan plan;
