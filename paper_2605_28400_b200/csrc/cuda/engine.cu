@@ -378,6 +378,7 @@ struct DeviceCtx {
   DevBuf<int32_t> d_score, d_end;
   DevBuf<unsigned long long> d_key;
   std::vector<std::unique_ptr<BucketLaunch>> plan_pool;  // pipelined path launch plans (grow-only)
+  ta_batch* oneshot = nullptr;  // reused batch object of the one-shot rows / affine path (never freed)
 };
 
 std::mutex g_ctx_mu;
@@ -503,6 +504,12 @@ struct ta_batch {
   // contents, lanes and mode are unchanged)
   std::vector<std::unique_ptr<BucketLaunch>> plan_cache;
   std::vector<ta::AffEntry> aff_cache;  // affine path: kernel per cached plan
+  std::vector<std::unique_ptr<BucketLaunch>> rows_pool;  // rows path: per-chunk launch plans (grow-only)
+  // staging of ta_batch_create (kept so a reused batch allocates nothing)
+  DevBuf<char> s_ascii;
+  DevBuf<int64_t> s_src;
+  DevBuf<int32_t> s_len, s_bad;
+  DevBuf<uint32_t> s_dst;
   std::string plan_key;
   int last_mode = -1;
   bool last_rows = false;
@@ -850,13 +857,21 @@ int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st,
   return TA_OK;
 }
 
+// One launch plan per call from the batch's pool (grow-only buffers).
+BucketLaunch* rows_plan(ta_batch* bt, size_t* used) {
+  if (*used == bt->rows_pool.size()) bt->rows_pool.push_back(std::make_unique<BucketLaunch>());
+  BucketLaunch* bl = bt->rows_pool[(*used)++].get();
+  bl->wave = false;
+  bl->rounds.clear();
+  return bl;
+}
+
 int launch_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
-                  bool trace, const ta::WaveArgs& base, cudaStream_t st, int64_t* launches) {
-  BucketLaunch bl;
-  if (int rc = prepare_bucket(bt, ids, grid, lanes, mode, trace, st, &bl)) return rc;
-  if (int rc = launch_prepared(&bl, base, st, launches)) return rc;
-  TA_CK(cudaStreamSynchronize(st));  // bl's buffers die here
-  bt->stats.padded_cells += bl.padded;
+                  bool trace, const ta::WaveArgs& base, cudaStream_t st, int64_t* launches, size_t* used) {
+  BucketLaunch* bl = rows_plan(bt, used);
+  if (int rc = prepare_bucket(bt, ids, grid, lanes, mode, trace, st, bl)) return rc;
+  if (int rc = launch_prepared(bl, base, st, launches)) return rc;
+  bt->stats.padded_cells += bl->padded;
   return TA_OK;
 }
 
@@ -1009,7 +1024,8 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
     // records: (a+1) * blocks * T tile-slices of kAffRec words per triplet, chunked by free HBM
     size_t free_b = 0, total_b = 0;
     TA_CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b) * 0.5));
+    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b + bt->d_dirs.cap * 16) * 0.5));
+    size_t pool_used = 0;
     bt->plan_key.clear();
     TA_CK(cudaEventRecord(bt->ev0, st));
     for (int w = 0; w < 2; ++w) {
@@ -1038,11 +1054,11 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
         ta::AffArgs args = base;
         args.dirs = reinterpret_cast<uint32_t*>(bt->d_dirs.ptr);
         args.dir_off = bt->d_diroff.ptr;
-        BucketLaunch bl;
+        BucketLaunch* bl = rows_plan(bt, &pool_used);
         ta::AffEntry ae;
-        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1, st, &bl, &ae)) return rc;
-        if (int rc = aff_launch(&bl, ae, args, st, &launches)) return rc;
-        bt->stats.padded_cells += bl.padded;
+        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1, st, bl, &ae)) return rc;
+        if (int rc = aff_launch(bl, ae, args, st, &launches)) return rc;
+        bt->stats.padded_cells += bl->padded;
         if (int rc = decode(chunk)) return rc;
         TA_CK(bt->d_ids.reserve(chunk.size()));
         TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
@@ -1206,7 +1222,8 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     // Direction-cube chunks: (a+1) * G^2 tile-slices of 64 B per triplet.
     size_t free_b = 0, total_b = 0;
     TA_CK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b) * 0.5));
+    const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b + bt->d_dirs.cap * 16) * 0.5));
+    size_t pool_used = 0;
     TA_CK(cudaEventRecord(bt->ev0, st));
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       const std::vector<int32_t>& ids = buckets[size_t(gi)];
@@ -1234,7 +1251,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
         ta::WaveArgs args = base;
         args.dirs = bt->d_dirs.ptr;
         args.dir_off = bt->d_diroff.ptr;
-        if (int rc = launch_bucket(bt, chunk, g, 1, opt.mode, true, args, st, &launches)) return rc;
+        if (int rc = launch_bucket(bt, chunk, g, 1, opt.mode, true, args, st, &launches, &pool_used)) return rc;
         if (opt.mode != TA_GLOBAL) {
           TA_CK(bt->d_ids.reserve(chunk.size()));
           TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
@@ -1573,14 +1590,14 @@ int ta_device_count(int* count) {
   return TA_OK;
 }
 
-int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_t n,
-                    ta_batch** out, void* stream) {
-  *out = nullptr;
-  if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
-  DeviceCtx* ctx = nullptr;
-  if (int rc = get_ctx(device, &ctx)) return rc;
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
-  auto bt = std::make_unique<ta_batch>();
+// (Re)initialises a batch object with new inputs; device buffers are reused
+// (grow-only), so a batch object kept by the caller allocates nothing.
+static int batch_init(ta_batch* bt, DeviceCtx* ctx, int device, const char* seqs, const int64_t* offsets, int64_t n,
+               cudaStream_t st) {
+  bt->plan_cache.clear();
+  bt->aff_cache.clear();
+  bt->plan_key.clear();
+  bt->stats = ta_stats{};
   bt->device = device;
   bt->ctx = ctx;
   bt->n = n;
@@ -1624,10 +1641,11 @@ int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_
   TA_CK(bt->d_status.reserve(size_t(n)));
   TA_CK(bt->d_key.reserve(size_t(n)));
   if (n > 0) {
-    DevBuf<char> ascii;
-    DevBuf<int64_t> d_src;
-    DevBuf<int32_t> d_len, d_bad;
-    DevBuf<uint32_t> d_dst;
+    DevBuf<char>& ascii = bt->s_ascii;
+    DevBuf<int64_t>& d_src = bt->s_src;
+    DevBuf<int32_t>& d_len = bt->s_len;
+    DevBuf<int32_t>& d_bad = bt->s_bad;
+    DevBuf<uint32_t>& d_dst = bt->s_dst;
     TA_CK(ascii.reserve(size_t(bytes) + 1));
     TA_CK(d_src.reserve(size_t(3 * n)));
     TA_CK(d_len.reserve(size_t(3 * n)));
@@ -1651,6 +1669,18 @@ int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_
     for (int64_t t = 0; t < n; ++t)
       if (bad[size_t(t)]) bt->pre_status[size_t(t)] = TA_ERR_PARSE;
   }
+  return TA_OK;
+}
+
+int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_t n,
+                    ta_batch** out, void* stream) {
+  *out = nullptr;
+  if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
+  DeviceCtx* ctx = nullptr;
+  if (int rc = get_ctx(device, &ctx)) return rc;
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  auto bt = std::make_unique<ta_batch>();
+  if (int rc = batch_init(bt.get(), ctx, device, seqs, offsets, n, st)) return rc;
   *out = bt.release();
   return TA_OK;
 }
@@ -1708,10 +1738,15 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
     return align_scores_pipelined(ctx, seqs, offsets, n, *scheme, *opt, out, st);
   }
-  ta_batch* bt = nullptr;
-  if (int rc = ta_batch_create(device, seqs, offsets, n, &bt, stream)) return rc;
-  std::unique_ptr<ta_batch, void (*)(ta_batch*)> guard(bt, ta_batch_destroy);
-  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : bt->ctx->stream;
+  // One cached batch object per device: its device buffers (sequences,
+  // results, direction records, launch plans) are reused call after call.
+  DeviceCtx* ctx = nullptr;
+  if (int rc = get_ctx(device, &ctx)) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+  if (!ctx->oneshot) ctx->oneshot = new ta_batch();
+  ta_batch* bt = ctx->oneshot;
+  if (int rc = batch_init(bt, ctx, device, seqs, offsets, n, st)) return rc;
   if (!opt->with_rows) {
     if (int rc = run_impl(bt, *scheme, *opt, st, nullptr)) return rc;
     return ta_batch_fetch(bt, out, stream);
