@@ -49,6 +49,8 @@ struct AffArgs {
   uint32_t one;
   int32_t* __restrict__ faces;              // block faces, 4 values per position
   const int64_t* __restrict__ face_off;     // per stream, in words
+  const int64_t* __restrict__ wave_base;    // wave mode: per triplet, its rings in 8-byte entries
+  uint32_t epoch;                           // wave mode: launch epoch (high half of the tags)
 };
 
 constexpr int kAffN = 5;  // tile side of the affine kernel
@@ -61,6 +63,12 @@ __host__ __device__ inline int64_t aff_face_words(int a, int bk, int gn) {
   return (int64_t(bk) * (a + 1) * (gn + 1) + int64_t(a + 1) * gn) * 4;
 }
 
+// Wave mode (blocks of a long triplet on different CTAs, wavefront.cuh's
+// scheme): per block a down and a right ring [a + 1][G][kAffSegE] of (value,
+// tag) 8-byte entries; a segment holds N + 1 positions x 4 values.
+constexpr int kAffSegE = 24;  // 4 x (kAffN + 1) entries = 192 B = 12 x 16 B
+__host__ __device__ inline int64_t aff_wave_block_entries(int a, int g) { return int64_t(2) * (a + 1) * g * kAffSegE; }
+
 template <int N, int G, int LANES>
 struct AffSmem {
   static constexpr int T = G * G;
@@ -71,15 +79,19 @@ struct AffSmem {
   static constexpr size_t kX = (size_t(2) * XW * (T + 1) * 4 + 15) / 16 * 16;
   static constexpr int kLaneFields = 12;
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
-  static constexpr size_t kStage = size_t(LANES) * 2 * G * (N + 1) * 16;
+  static constexpr size_t kStage = size_t(LANES) * 2 * G * kAffSegE * 8;  // either face layout
   static constexpr size_t kBar = 16;
   static constexpr int kSlots = 64;
   static constexpr size_t kBest = size_t(LANES) * kSlots * 12;
   static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane + kStage + kBar + kBest;
 };
 
-template <int N, int G, int LANES, int MODE, bool TRACE, bool BLOCKS>
+template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
 __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
+  // BLK: 0 single block, 1 sequential block items, 2 wave mode (tagged rings)
+  constexpr bool BLOCKS = BLK != 0;
+  constexpr bool WAVE = BLK == 2;
+  static_assert(4 * (N + 1) <= kAffSegE, "ring segment too small");
   static_assert(!TRACE || LANES == 1, "TRACE uses int32 lanes");
   using Ops = LaneOps<LANES>;
   using SM = AffSmem<N, G, LANES>;
@@ -169,8 +181,10 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   auto fetch = [&](int l, int it, int iend) -> LaneLoad {
     int id = -1, a_ = 0, b_ = -1, c_ = -1, len = 0x3FFFFFFF, J = 0, K = 0, Bj = 1, Bk = 1;
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
-    if (it < iend) {
-      const int4 rec = __ldg(args.items + it);
+    int4 rec = make_int4(-1, 0, 0x3FFFFFFF, 0x00010001);
+    if (it < iend) rec = __ldg(args.items + it);
+    if (rec.x < 0 && it < iend) len = rec.z;  // null item (wave partner): idle for len slices
+    if (rec.x >= 0) {
       id = rec.x;
       J = rec.y >> 16;
       K = rec.y & 0xFFFF;
@@ -196,7 +210,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
-    uint32_t f = id >= 0 ? 0u : kDone;
+    uint32_t f = (id >= 0 || it < iend) ? 0u : kDone;
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
     if (id >= 0 && J > 0) f |= kInTop;
     if (id >= 0 && K > 0) f |= kInLeft;
@@ -314,6 +328,48 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           for (int l = 0; l < LANES; ++l) {
             const bool ok = si[l] <= la[l];
             const uint32_t m = Ops::mask(l);
+            if constexpr (WAVE) {
+              // tagged rings: only a lane with real cells in this tile waits
+              const bool real = LS(l, kTid) >= 0 && LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 &&
+                                LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
+              if (!ok || !real) continue;
+              const uint32_t want = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
+              const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+              const int a1 = la[l] + 1;
+              const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+              auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
+                uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kAffSegE + e];
+                while (v.y != want) {
+                  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(src + e));
+                }
+                return static_cast<int32_t>(v.x);
+              };
+              if (r == 0 && (flags[l] & kInTop)) {
+                const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kAffSegE;
+#pragma unroll
+                for (int q = 0; q <= N; ++q) {  // (B, E2, E4, E6) at k = cN + q - 1
+                  if (q < N) {
+                    cB[0][q] = lop_sel(cB[0][q], Ops::splat(take(cc, src, 4 * q)), m);
+                    cE4[0][q] = lop_sel(cE4[0][q], Ops::splat(take(cc, src, 4 * q + 2)), m);
+                  }
+                  if (q > 0) {
+                    cE2[0][q] = lop_sel(cE2[0][q], Ops::splat(take(cc, src, 4 * q + 1)), m);
+                    cE6[0][q] = lop_sel(cE6[0][q], Ops::splat(take(cc, src, 4 * q + 3)), m);
+                  }
+                }
+              }
+              if (cc == 0 && (flags[l] & kInLeft)) {
+                const uint64_t* src = fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kAffSegE;
+#pragma unroll
+                for (int p = 0; p < N; ++p) {  // (B, E3, E4, E7) at j = rN + p
+                  cB[p + 1][0] = lop_sel(cB[p + 1][0], Ops::splat(take(G + r, src, 4 * p)), m);
+                  cE3[p + 1][0] = lop_sel(cE3[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 1)), m);
+                  cE4[p + 1][0] = lop_sel(cE4[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 2)), m);
+                  cE7[p + 1][0] = lop_sel(cE7[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 3)), m);
+                }
+              }
+              continue;
+            }
             if (r == 0 && (flags[l] & kInTop) && ok) {
               const int4* st = reinterpret_cast<const int4*>(stage) + (l * 2 * G + cc) * (N + 1);
 #pragma unroll
@@ -507,6 +563,35 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           const bool rt = cc == G - 1 && (flags[l] & kOutRight);
           if (!dn && !rt) continue;
           const int a1 = la[l] + 1;
+          if constexpr (WAVE) {
+            const uint32_t tag = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
+            uint2* fb = reinterpret_cast<uint2*>(reinterpret_cast<uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)]);
+            const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+            auto put = [&](uint2* d, int e, uint32_t v) { d[e] = make_uint2(static_cast<uint32_t>(Ops::lane(v, l)), tag); };
+            if (dn) {  // segment cc: q = 0 is the corner (this tile's halo), q = 1..N its bottom row
+              uint2* d = fb + ((int64_t(blk) * 2 * a1 + si[l]) * G + cc) * kAffSegE;
+              put(d, 0, cB[N][0]);
+              put(d, 2, cE4[N][0]);
+#pragma unroll
+              for (int q = 1; q <= N; ++q) {
+                put(d, 4 * q, cB[N][q]);
+                put(d, 4 * q + 1, cE2[N][q]);
+                put(d, 4 * q + 2, cE4[N][q]);
+                put(d, 4 * q + 3, cE6[N][q]);
+              }
+            }
+            if (rt) {  // segment r: positions p = 0..N-1 of this tile's right column
+              uint2* d = fb + (((int64_t(blk) * 2 + 1) * a1 + si[l]) * G + r) * kAffSegE;
+#pragma unroll
+              for (int p = 0; p < N; ++p) {
+                put(d, 4 * p, cB[p + 1][N]);
+                put(d, 4 * p + 1, cE3[p + 1][N]);
+                put(d, 4 * p + 2, cE4[p + 1][N]);
+                put(d, 4 * p + 3, cE7[p + 1][N]);
+              }
+            }
+            continue;
+          }
           int4* fb = reinterpret_cast<int4*>(args.faces + args.face_off[sbase + l]);
           if (dn) {  // own cells Q = 1..N at positions cN + Q; tile 0 also the corner (its halo)
             int4* d = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
@@ -718,6 +803,25 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       for (int l = 0; l < LANES; ++l) {
         if ((flags[l] & kDone) || si[l] > la[l]) continue;
         const int a1 = la[l] + 1;
+        if constexpr (WAVE) {
+          if (LS(l, kTid) < 0 || !(flags[l] & (kInTop | kInLeft))) continue;
+          const uint64_t* fw = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+          const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+          auto fetch_seg = [&](int seg, const uint64_t* src) {
+            uint64_t* dst = reinterpret_cast<uint64_t*>(stage) + (l * 2 * G + seg) * kAffSegE;
+#pragma unroll
+            for (int v = 0; v < kAffSegE / 2; ++v)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                               static_cast<uint32_t>(__cvta_generic_to_shared(dst + 2 * v))),
+                           "l"(src + 2 * v)
+                           : "memory");
+          };
+          if (r == 0 && (flags[l] & kInTop))
+            fetch_seg(cc, fw + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kAffSegE);
+          if (cc == 0 && (flags[l] & kInLeft))
+            fetch_seg(G + r, fw + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kAffSegE);
+          continue;
+        }
         const int4* fb = reinterpret_cast<const int4*>(args.faces + args.face_off[sbase + l]);
         if (r == 0 && (flags[l] & kInTop)) {
           const int4* src = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;

@@ -659,7 +659,7 @@ struct WavePlan {
 
 void plan_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, const std::vector<int32_t>& b,
                const std::vector<int32_t>& c, int max_ctas, int lanes, int grid, int64_t n, WavePlan* out,
-               int* ctas_out) {
+               int* ctas_out, int tile_n = ta::kTileN, bool affine = false) {
   struct Blk {
     int d, id, J, K;
   };
@@ -667,15 +667,16 @@ void plan_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, c
   out->base.assign(size_t(n), 0);
   out->entries = 0;
   for (int32_t id : ids) {
-    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid);
+    const Blocks bl = blocks_of(b[size_t(id)], c[size_t(id)], grid, tile_n);
     out->base[size_t(id)] = out->entries;
-    out->entries += int64_t(bl.bj) * bl.bk * ta::wave_block_entries(a[size_t(id)], grid);
+    out->entries += int64_t(bl.bj) * bl.bk *
+                    (affine ? ta::aff_wave_block_entries(a[size_t(id)], grid) : ta::wave_block_entries(a[size_t(id)], grid));
     for (int J = 0; J < bl.bj; ++J)
       for (int K = 0; K < bl.bk; ++K) blks.push_back(Blk{J + K, id, J, K});
   }
   std::stable_sort(blks.begin(), blks.end(), [](const Blk& x, const Blk& y) { return x.d < y.d; });
   auto rec = [&](const Blk& x) {
-    const Blocks bl = blocks_of(b[size_t(x.id)], c[size_t(x.id)], grid);
+    const Blocks bl = blocks_of(b[size_t(x.id)], c[size_t(x.id)], grid, tile_n);
     return make_int4(x.id, (x.J << 16) | x.K, a[size_t(x.id)] + 1, (bl.bj << 16) | bl.bk);
   };
   std::vector<std::pair<int4, int4>> pairs;  // (lane 0, lane 1); lane 1 may be a null item
@@ -896,14 +897,42 @@ bool aff_s16_ok(const ta_scheme& s, int64_t max_bound) {
   return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kAffN + 2 * int64_t(-s.gap_open) <= 32000;
 }
 
-int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mode, bool trace, bool blocks,
+int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mode, bool trace, int blk,
                 cudaStream_t st, BucketLaunch* bl, ta::AffEntry* ae) {
-  *ae = ta::lookup_affine(lanes, mode, trace, blocks);
+  *ae = ta::lookup_affine(lanes, mode, trace, blk);
   if (!ae->fn) return fail(TA_ERR_LOGIC, "no affine kernel instantiation");
   TA_CK(cudaFuncSetAttribute(ae->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ae->smem)));
   int per_sm = 0;
   TA_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ae->fn, ae->threads, ae->smem));
   if (per_sm < 1) return fail(TA_ERR_CUDA, "affine kernel does not fit on an SM");
+  bl->wave = blk == 2;
+  bl->rounds.clear();
+  if (blk == 2) {  // wave mode: blocks spread over all CTAs, tagged rings (see plan_wave)
+    WavePlan plan;
+    int ctas = 0;
+    plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, ta::kAffG, int64_t(bt->a.size()), &plan, &ctas,
+              ta::kAffN, true);
+    bl->grid = ta::kAffG;
+    bl->lanes = lanes;
+    bl->mode = mode;
+    bl->ctas = ctas;
+    bl->rounds = plan.rounds;
+    TA_CK(bl->items.reserve(plan.items.size()));
+    TA_CK(bl->soff.reserve(plan.soff.size()));
+    TA_CK(bl->steps.reserve(plan.steps.size()));
+    TA_CK(bl->faces.reserve(size_t(plan.entries) * 2 + 4));
+    TA_CK(bl->wave_base.reserve(plan.base.size()));
+    TA_CK(bl->face_off.reserve(1));
+    bl->face_bytes = plan.entries * 8;
+    TA_CK(cudaMemsetAsync(bl->faces.ptr, 0, size_t(bl->face_bytes), st));
+    bl->epoch = 0;
+    TA_CK(cudaMemcpyAsync(bl->wave_base.ptr, plan.base.data(), plan.base.size() * 8, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
+    TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
+    bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * ta::kAffN * ta::kAffN;
+    return TA_OK;
+  }
   const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
   bl->grid = ta::kAffG;
   bl->lanes = lanes;
@@ -933,6 +962,23 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
   args.cta_steps = bl->steps.ptr;
   args.faces = bl->faces.ptr;
   args.face_off = bl->face_off.ptr;
+  if (bl->wave) {
+    if (++bl->epoch >= 65536u) {  // tags would repeat: clear the rings
+      TA_CK(cudaMemsetAsync(bl->faces.ptr, 0, size_t(bl->face_bytes), st));
+      bl->epoch = 1;
+    }
+    args.wave_base = bl->wave_base.ptr;
+    args.epoch = bl->epoch;
+    for (const WaveRound& rd : bl->rounds) {
+      ta::AffArgs ra = args;
+      ra.stream_off = bl->soff.ptr + rd.soff_at;
+      ra.cta_steps = bl->steps.ptr + rd.steps_at;
+      ae.fn<<<rd.ctas, ae.threads, ae.smem, st>>>(ra);
+      TA_CK(cudaGetLastError());
+      *launches += 1;
+    }
+    return TA_OK;
+  }
   ae.fn<<<bl->ctas, ae.threads, ae.smem, st>>>(args);
   TA_CK(cudaGetLastError());
   *launches += 1;
@@ -942,7 +988,7 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
 int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
                const std::vector<int32_t>& all_ok, bool rows) {
   const int64_t n = bt->n;
-  std::vector<int32_t> single, multi;
+  std::vector<int32_t> single, multi, wave;
   int64_t maxb = 0;
   for (int32_t id : all_ok) {
     const int32_t B = bt->b[size_t(id)], C = bt->c[size_t(id)];
@@ -950,6 +996,12 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
     maxb = std::max(maxb, aff_lane_bound(scheme, bt->a[size_t(id)], B, C));
   }
   const int lanes = (!rows && aff_s16_ok(scheme, maxb)) ? 2 : 1;
+  // few long triplets: spread their blocks over all CTAs (wave mode)
+  if (!rows && !multi.empty() && int64_t(multi.size()) * 2 <= int64_t(bt->ctx->sms) * lanes) {
+    bool ok = true;
+    for (int32_t id : multi) ok &= bt->a[size_t(id)] + 1 < 65535;
+    if (ok) wave.swap(multi);
+  }
   ta::AffArgs base{};
   base.seq = bt->seq.ptr;
   base.desc = bt->d_desc.ptr;
@@ -989,12 +1041,12 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
       bt->plan_cache.clear();
       bt->aff_cache.clear();
       bt->plan_key.clear();
-      for (int w = 0; w < 2; ++w) {
-        const std::vector<int32_t>& part = w ? multi : single;
+      for (int w = 0; w < 3; ++w) {
+        const std::vector<int32_t>& part = w == 2 ? wave : w ? multi : single;
         if (part.empty()) continue;
         bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
         bt->aff_cache.emplace_back();
-        if (int rc = aff_prepare(bt, part, lanes, opt.mode, false, w == 1, st, bt->plan_cache.back().get(),
+        if (int rc = aff_prepare(bt, part, lanes, opt.mode, false, w, st, bt->plan_cache.back().get(),
                                  &bt->aff_cache.back()))
           return rc;
       }
@@ -1056,7 +1108,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
         args.dir_off = bt->d_diroff.ptr;
         BucketLaunch* bl = rows_plan(bt, &pool_used);
         ta::AffEntry ae;
-        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1, st, bl, &ae)) return rc;
+        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1 ? 1 : 0, st, bl, &ae)) return rc;
         if (int rc = aff_launch(bl, ae, args, st, &launches)) return rc;
         bt->stats.padded_cells += bl->padded;
         if (int rc = decode(chunk)) return rc;

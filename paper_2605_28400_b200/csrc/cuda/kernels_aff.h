@@ -19,12 +19,15 @@ struct AffEntry {
   int threads = 0;
 };
 
-// trace requires lanes == 1
+// trace requires lanes == 1; blk: 0 single block, 1 sequential block items,
+// 2 wave mode (no trace)
 AffEntry affine_kernel_single(int lanes, int mode, bool trace);
 AffEntry affine_kernel_blocks(int lanes, int mode, bool trace);
+AffEntry affine_kernel_wave(int lanes, int mode, bool trace);
 
-inline AffEntry lookup_affine(int lanes, int mode, bool trace, bool blocks) {
-  return blocks ? affine_kernel_blocks(lanes, mode, trace) : affine_kernel_single(lanes, mode, trace);
+inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
+  if (blk == 2) return trace ? AffEntry{} : affine_kernel_wave(lanes, mode, false);
+  return blk ? affine_kernel_blocks(lanes, mode, trace) : affine_kernel_single(lanes, mode, trace);
 }
 
 }  // namespace ta
@@ -35,6 +38,7 @@ inline AffEntry lookup_affine(int lanes, int mode, bool trace, bool blocks) {
 #define TA_DEFINE_AFF_TABLE(NAME, BL)                          \
   namespace ta {                                               \
   AffEntry NAME(int lanes, int mode, bool trace) {             \
+    if (trace && BL == 2) return {};                           \
     if (trace) {                                               \
       if (lanes != 1) return {};                               \
       switch (mode) {                                          \

@@ -149,3 +149,19 @@ def test_cli_gap_open_matches_oracle(gpu_engine, oracle, tmp_path):
             f = line.split(",")
             want = oracle.affine(trips[x], (1, -1, -2, -3), mode)
             assert f[1] == name and int(f[2]) == want["score"] and [int(v) for v in f[3:6]] == want["end"], line
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_affine_wave_pairs_of_different_triplets(gpu_engine, oracle, mode):
+    """Affine wave mode (few long triplets spread over all CTAs), pairing
+    blocks of different triplets with equal a but different b, c."""
+    rng = np.random.default_rng(77 + mode)
+    trips = []
+    for b, c in [(165, 300), (310, 170), (200, 200), (330, 161), (250, 180)]:
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (180, b, c)))
+    sch = (1, -1, -2, -3)
+    out = run(trips, sch, mode)
+    for x, t in enumerate(trips):
+        want = oracle.affine(t, sch, mode)
+        assert int(out["status"][x]) == 0
+        assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
