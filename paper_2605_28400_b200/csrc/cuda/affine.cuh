@@ -69,7 +69,7 @@ __host__ __device__ inline int64_t aff_face_words(int a, int bk, int gn) {
 constexpr int kAffSegE = 24;  // 4 x (kAffN + 1) entries = 192 B = 12 x 16 B
 __host__ __device__ inline int64_t aff_wave_block_entries(int a, int g) { return int64_t(2) * (a + 1) * g * kAffSegE; }
 
-template <int N, int G, int LANES>
+template <int N, int G, int LANES, int BLK>
 struct AffSmem {
   static constexpr int T = G * G;
   static constexpr int NN = N * N;
@@ -79,7 +79,10 @@ struct AffSmem {
   static constexpr size_t kX = (size_t(2) * XW * (T + 1) * 4 + 15) / 16 * 16;
   static constexpr int kLaneFields = 12;
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
-  static constexpr size_t kStage = size_t(LANES) * 2 * G * kAffSegE * 8;  // either face layout
+  // prefetched faces: int4 per position (sequential blocks) or tagged ring
+  // segments (wave); sized per variant so the L1 carve-out stays as large as
+  // possible (the face prefetch of sequential blocks goes through L1)
+  static constexpr size_t kStage = BLK == 2 ? size_t(LANES) * 2 * G * kAffSegE * 8 : size_t(LANES) * 2 * G * (N + 1) * 16;
   static constexpr size_t kBar = 16;
   static constexpr int kSlots = 64;
   static constexpr size_t kBest = size_t(LANES) * kSlots * 12;
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   static_assert(4 * (N + 1) <= kAffSegE, "ring segment too small");
   static_assert(!TRACE || LANES == 1, "TRACE uses int32 lanes");
   using Ops = LaneOps<LANES>;
-  using SM = AffSmem<N, G, LANES>;
+  using SM = AffSmem<N, G, LANES, BLK>;
   constexpr int T = SM::T;
   constexpr int NN = SM::NN;
   constexpr int XW = SM::XW;
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
     int4 rec = make_int4(-1, 0, 0x3FFFFFFF, 0x00010001);
     if (it < iend) rec = __ldg(args.items + it);
-    if (rec.x < 0 && it < iend) len = rec.z;  // null item (wave partner): idle for len slices
+    if (WAVE && rec.x < 0 && it < iend) len = rec.z;  // null item (wave partner): idle for len slices
     if (rec.x >= 0) {
       id = rec.x;
       J = rec.y >> 16;
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
-    uint32_t f = (id >= 0 || it < iend) ? 0u : kDone;
+    uint32_t f = (id >= 0 || (WAVE && it < iend)) ? 0u : kDone;
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
     if (id >= 0 && J > 0) f |= kInTop;
     if (id >= 0 && K > 0) f |= kInLeft;

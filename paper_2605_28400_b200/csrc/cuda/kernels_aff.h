@@ -33,7 +33,7 @@ inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
 }  // namespace ta
 
 #define TA_AFF_ENTRY(L, M, TR, BL) \
-  AffEntry{&affine_kernel<kAffN, kAffG, L, M, TR, BL>, AffSmem<kAffN, kAffG, L>::bytes, kAffG * kAffG}
+  AffEntry{&affine_kernel<kAffN, kAffG, L, M, TR, BL>, AffSmem<kAffN, kAffG, L, BL>::bytes, kAffG * kAffG}
 
 #define TA_DEFINE_AFF_TABLE(NAME, BL)                          \
   namespace ta {                                               \
