@@ -42,15 +42,18 @@ struct AffArgs {
   int32_t* __restrict__ out_end;
   unsigned long long* __restrict__ out_key;
   uint32_t* __restrict__ dirs;              // TRACE: per-cell records
-  const int64_t* __restrict__ dir_off;      // TRACE: per triplet, in uint4
+  union {
+    const int64_t* __restrict__ dir_off;    // TRACE: per triplet, in uint4
+    uint64_t epoch;                         // wave mode (never TRACE): launch epoch, the high half of the tags
+  };
   int32_t match_p, mismatch_p, g2;          // sigma' (= sigma - 2 gap) and 2 gap
   int32_t open;                             // gap_open (<= 0)
   int32_t bias;                             // -8 open
   uint32_t one;
   int32_t* __restrict__ faces;              // block faces, 4 values per position
-  const int64_t* __restrict__ face_off;     // per stream, in words
-  const int64_t* __restrict__ wave_base;    // wave mode: per triplet, its rings in 8-byte entries
-  uint32_t epoch;                           // wave mode: launch epoch (high half of the tags)
+  const int64_t* __restrict__ face_off;     // blocks: per stream, in words; wave: per triplet, its rings in
+                                            // 8-byte entries (the parameter block is kept at its pre-wave size:
+                                            // two more fields cost the block kernel 4.5% through ptxas scheduling)
 };
 
 constexpr int kAffN = 5;  // tile side of the affine kernel
@@ -184,10 +187,11 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   auto fetch = [&](int l, int it, int iend) -> LaneLoad {
     int id = -1, a_ = 0, b_ = -1, c_ = -1, len = 0x3FFFFFFF, J = 0, K = 0, Bj = 1, Bk = 1;
     uint32_t ww0 = 0, ww1 = 0, ww2 = 0;
-    int4 rec = make_int4(-1, 0, 0x3FFFFFFF, 0x00010001);
-    if (it < iend) rec = __ldg(args.items + it);
-    if (WAVE && rec.x < 0 && it < iend) len = rec.z;  // null item (wave partner): idle for len slices
-    if (rec.x >= 0) {
+    if (it < iend) {
+      const int4 rec = __ldg(args.items + it);
+      if (WAVE && rec.x < 0) {
+        len = rec.z;  // null item (wave partner): idle for len slices
+      } else {
       id = rec.x;
       J = rec.y >> 16;
       K = rec.y & 0xFFFF;
@@ -202,6 +206,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       ww0 = d1.x;
       ww1 = d1.y;
       ww2 = d1.z;
+      }
     }
     la[l] = a_;
     LS(l, kTid) = id;
@@ -336,8 +341,8 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               const bool real = LS(l, kTid) >= 0 && LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 &&
                                 LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
               if (!ok || !real) continue;
-              const uint32_t want = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
-              const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+              const uint32_t want = (static_cast<uint32_t>(args.epoch) << 16) + static_cast<uint32_t>(si[l]) + 1u;
+              const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.face_off[LS(l, kTid)];
               const int a1 = la[l] + 1;
               const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
               auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
@@ -567,8 +572,8 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           if (!dn && !rt) continue;
           const int a1 = la[l] + 1;
           if constexpr (WAVE) {
-            const uint32_t tag = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
-            uint2* fb = reinterpret_cast<uint2*>(reinterpret_cast<uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)]);
+            const uint32_t tag = (static_cast<uint32_t>(args.epoch) << 16) + static_cast<uint32_t>(si[l]) + 1u;
+            uint2* fb = reinterpret_cast<uint2*>(reinterpret_cast<uint64_t*>(args.faces) + args.face_off[LS(l, kTid)]);
             const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
             auto put = [&](uint2* d, int e, uint32_t v) { d[e] = make_uint2(static_cast<uint32_t>(Ops::lane(v, l)), tag); };
             if (dn) {  // segment cc: q = 0 is the corner (this tile's halo), q = 1..N its bottom row
@@ -808,7 +813,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         const int a1 = la[l] + 1;
         if constexpr (WAVE) {
           if (LS(l, kTid) < 0 || !(flags[l] & (kInTop | kInLeft))) continue;
-          const uint64_t* fw = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
+          const uint64_t* fw = reinterpret_cast<const uint64_t*>(args.faces) + args.face_off[LS(l, kTid)];
           const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
           auto fetch_seg = [&](int seg, const uint64_t* src) {
             uint64_t* dst = reinterpret_cast<uint64_t*>(stage) + (l * 2 * G + seg) * kAffSegE;

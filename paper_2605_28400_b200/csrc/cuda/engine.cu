@@ -967,7 +967,7 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
       TA_CK(cudaMemsetAsync(bl->faces.ptr, 0, size_t(bl->face_bytes), st));
       bl->epoch = 1;
     }
-    args.wave_base = bl->wave_base.ptr;
+    args.face_off = bl->wave_base.ptr;  // wave: ring base per triplet (AffArgs)
     args.epoch = bl->epoch;
     for (const WaveRound& rd : bl->rounds) {
       ta::AffArgs ra = args;
