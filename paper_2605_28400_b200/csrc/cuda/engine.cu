@@ -452,9 +452,9 @@ struct LanePlan {
 
 // Largest in-grid cell value (gap-shifted, >= 0) a triplet can produce, incl.
 // padding cells and idle slices: (match + |g2|) * (slices + j extent + k extent).
-int64_t lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c, int grid) {
+int64_t lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c, int grid, int tile_n = ta::kTileN) {
   const int g2 = 2 * s.gap;
-  const int64_t gn = int64_t(grid) * ta::kTileN;
+  const int64_t gn = int64_t(grid) * tile_n;
   const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
   const int64_t slices = std::max<int64_t>(a + 1, grid + 2 + (grid * grid + 31) / 32);
   return int64_t(s.match - g2) * (slices + ej + ek);
@@ -752,9 +752,52 @@ void split_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, 
   }
 }
 
+// Multi-block triplets of the largest grid whose (j, k) extents pad less in
+// 128-wide blocks (8 x 8 tiles) than in 160-wide ones, weighting a 128-block
+// cell by the measured per-cell cost ratio of the two kernels (smaller tiles
+// amortise the per-step work over 64 instead of 100 cells).  Example: 250 bp
+// (extent 251) pads to 2 x 2 blocks either way: 65536 vs 102400 cells/slice.
+double t8_cost_ratio() {
+  static const double r = [] {
+    const char* e = std::getenv("TA_T8_COST");
+    return e ? std::atof(e) : 1.2;  // measured: 2247 vs 2686 padded-cell GCUPS (C3)
+  }();
+  return r;
+}
+
+bool prefer_t8(int32_t b, int32_t c) {
+  const Blocks b10 = blocks_of(b, c, 16);
+  if (b10.bj * b10.bk <= 1) return false;
+  const Blocks b8 = blocks_of(b, c, 16, ta::kSmallTileN);
+  const double g10 = 16.0 * ta::kTileN, g8 = 16.0 * ta::kSmallTileN;
+  return double(b8.bj * b8.bk) * g8 * g8 * t8_cost_ratio() < double(b10.bj * b10.bk) * g10 * g10;
+}
+
+// Splits the largest grid's bucket into wave triplets, 128-wide-block
+// triplets (prefer_t8, with their own lane choice) and the rest.
+void split_largest(const std::vector<int32_t>& bucket, const std::vector<int32_t>& a, const std::vector<int32_t>& b,
+                   const std::vector<int32_t>& c, const ta_scheme& scheme, int lane_streams,
+                   std::vector<int32_t>* wave, std::vector<int32_t>* rest, std::vector<int32_t>* t8, int* lanes8) {
+  const int g = ta::kGridSizes[ta::kNumGrid - 1];
+  split_wave(bucket, a, b, c, g, lane_streams, wave, rest);
+  std::vector<int32_t> keep;
+  int64_t bound8 = 0;
+  t8->clear();
+  for (int32_t id : *rest) {
+    if (prefer_t8(b[size_t(id)], c[size_t(id)])) {
+      t8->push_back(id);
+      bound8 = std::max(bound8, lane_bound(scheme, a[size_t(id)], b[size_t(id)], c[size_t(id)], g, ta::kSmallTileN));
+    } else {
+      keep.push_back(id);
+    }
+  }
+  rest->swap(keep);
+  *lanes8 = s16_ok(scheme, bound8) ? 2 : 1;
+}
+
 // Host planning + upload for one bucket (outside any timed region).
 int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
-                   bool trace, cudaStream_t st, BucketLaunch* bl, bool wave = false) {
+                   bool trace, cudaStream_t st, BucketLaunch* bl, bool wave = false, int tile_n = ta::kTileN) {
   bl->grid = grid;
   bl->lanes = lanes;
   bl->mode = mode;
@@ -790,13 +833,15 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   }
   bool multi = false;
   for (int32_t id : ids) {
-    const Blocks b = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], grid);
+    const Blocks b = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], grid, tile_n);
     if (b.bj * b.bk > 1) {
       multi = true;
       break;
     }
   }
-  bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, multi ? 1 : 0);
+  if (tile_n != ta::kTileN && (grid != 16 || trace || !multi))
+    return fail(TA_ERR_LOGIC, "8 x 8 tiles exist for multi-block score items of grid 16 only");
+  bl->ke = tile_n != ta::kTileN ? ta::kernel_g16_t8(lanes, mode) : ta::lookup_kernel(grid, lanes, mode, trace, multi ? 1 : 0);
   const ta::KernelEntry& ke = bl->ke;
   if (!ke.fn) return fail(TA_ERR_LOGIC, "no kernel instantiation for grid " + std::to_string(grid));
   TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
@@ -813,7 +858,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
   bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
   StreamPlan plan;
-  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, grid, &plan);
+  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, grid, &plan, tile_n);
   if (plan.face_words > (int64_t(1) << 31)) return fail(TA_ERR_CAPACITY, "block-face scratch exceeds 2^31 words");
   TA_CK(bl->items.reserve(plan.items.size()));
   TA_CK(bl->soff.reserve(plan.soff.size()));
@@ -824,7 +869,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
-  bl->padded = plan.padded_slices * grid * grid * ta::kTileN * ta::kTileN;
+  bl->padded = plan.padded_slices * grid * grid * tile_n * tile_n;
   return TA_OK;
 }
 
@@ -1220,6 +1265,16 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     // plan key: mode + per-bucket (grid, lanes, ids) fingerprint
     std::string key = std::to_string(opt.mode);
     std::vector<int> lanes_of(ta::kNumGrid, 1);
+    // largest grid: wave triplets, 128-wide-block triplets (prefer_t8), the rest
+    const int gl = ta::kNumGrid - 1;
+    std::vector<int32_t> wave_ids, rest_ids, t8_ids;
+    int lanes8 = 1;
+    if (!buckets[size_t(gl)].empty()) {
+      const int l = s16_ok(scheme, max_bound_bucket[gl]) ? 2 : 1;
+      split_largest(buckets[size_t(gl)], bt->a, bt->b, bt->c, scheme, bt->ctx->sms * l, &wave_ids, &rest_ids, &t8_ids,
+                    &lanes8);
+      key += "|t8:" + std::to_string(t8_ids.size()) + ":" + std::to_string(lanes8);
+    }
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       if (buckets[size_t(gi)].empty()) continue;
       lanes_of[size_t(gi)] = s16_ok(scheme, max_bound_bucket[gi]) ? 2 : 1;
@@ -1233,15 +1288,20 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       bt->plan_key.clear();
       for (int gi = 0; gi < ta::kNumGrid; ++gi) {
         if (buckets[size_t(gi)].empty()) continue;
-        std::vector<int32_t> wave_ids, rest_ids;
-        split_wave(buckets[size_t(gi)], bt->a, bt->b, bt->c, ta::kGridSizes[gi], bt->ctx->sms * lanes_of[size_t(gi)],
-                   &wave_ids, &rest_ids);
-        for (int w = 0; w < 2; ++w) {
-          const std::vector<int32_t>& part = w ? wave_ids : rest_ids;
+        if (gi != gl) {
+          bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
+          if (int rc = prepare_bucket(bt, buckets[size_t(gi)], ta::kGridSizes[gi], lanes_of[size_t(gi)], opt.mode,
+                                      false, st, bt->plan_cache.back().get()))
+            return rc;
+          continue;
+        }
+        for (int w = 0; w < 3; ++w) {
+          const std::vector<int32_t>& part = w == 2 ? t8_ids : w ? wave_ids : rest_ids;
           if (part.empty()) continue;
           bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
-          if (int rc = prepare_bucket(bt, part, ta::kGridSizes[gi], lanes_of[size_t(gi)], opt.mode, false, st,
-                                      bt->plan_cache.back().get(), w == 1))
+          if (int rc = prepare_bucket(bt, part, ta::kGridSizes[gi], w == 2 ? lanes8 : lanes_of[size_t(gi)], opt.mode,
+                                      false, st, bt->plan_cache.back().get(), w == 1,
+                                      w == 2 ? ta::kSmallTileN : ta::kTileN))
             return rc;
         }
       }
@@ -1551,14 +1611,19 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     for (int gi = 0; gi < ta::kNumGrid && rc == TA_OK; ++gi) {
       if (buckets[size_t(gi)].empty()) continue;
       const int lanes = s16_ok(scheme, max_bound[gi]) ? 2 : 1;
-      std::vector<int32_t> wave_ids, rest_ids;
-      split_wave(buckets[size_t(gi)], shim.a, shim.b, shim.c, ta::kGridSizes[gi], ctx->sms * lanes, &wave_ids,
-                 &rest_ids);
-      for (int w = 0; w < 2 && rc == TA_OK; ++w) {
-        const std::vector<int32_t>& part = w ? wave_ids : rest_ids;
+      std::vector<int32_t> wave_ids, rest_ids, t8_ids;
+      int lanes8 = 1;
+      if (gi == ta::kNumGrid - 1)
+        split_largest(buckets[size_t(gi)], shim.a, shim.b, shim.c, scheme, ctx->sms * lanes, &wave_ids, &rest_ids,
+                      &t8_ids, &lanes8);
+      else
+        rest_ids = buckets[size_t(gi)];
+      for (int w = 0; w < 3 && rc == TA_OK; ++w) {
+        const std::vector<int32_t>& part = w == 2 ? t8_ids : w ? wave_ids : rest_ids;
         if (part.empty()) continue;
         BucketLaunch* bl = take_plan();
-        rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], lanes, opt.mode, false, ctx->copy, bl, w == 1);
+        rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], w == 2 ? lanes8 : lanes, opt.mode, false, ctx->copy, bl,
+                            w == 1, w == 2 ? ta::kSmallTileN : ta::kTileN);
         launch_now.push_back(bl);
       }
     }

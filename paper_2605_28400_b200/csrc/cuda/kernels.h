@@ -13,6 +13,7 @@ constexpr int kTileN = 10;                 // cells per tile side
 constexpr int kGridSizes[] = {4, 8, 12, 16};  // tile-grid sides (plane extent G*N)
 constexpr int kNumGrid = sizeof(kGridSizes) / sizeof(kGridSizes[0]);
 constexpr int kMaxExtent = 16 * kTileN;    // largest single-block plane side
+constexpr int kSmallTileN = 8;             // multi-block items in 128-wide blocks (16 x 16 tiles of 8 x 8)
 
 using WaveFn = void (*)(WaveArgs);
 
@@ -31,6 +32,9 @@ KernelEntry kernel_g8(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g12(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g16(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g16_wave(int lanes, int mode);
+// 16 x 16 grid of 8 x 8 tiles, multi-block items only (blk 1, no trace): long
+// triplets whose extents pad less in 128-wide blocks than in 160-wide ones
+KernelEntry kernel_g16_t8(int lanes, int mode);
 
 inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int blk) {
   if (blk == 2) return (grid == 16 && !trace) ? kernel_g16_wave(lanes, mode) : KernelEntry{};
@@ -84,6 +88,27 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
     if (blk != 0) return {};                                                           \
     return pick_##G<0>(lanes, mode, trace);                                            \
   }                                                                                    \
+  }
+
+#define TA_DEFINE_T8_TABLE()                                                                       \
+  namespace ta {                                                                                   \
+  KernelEntry kernel_g16_t8(int lanes, int mode) {                                                 \
+    constexpr int N8 = kSmallTileN;                                                                \
+    if (lanes == 1) {                                                                              \
+      switch (mode) {                                                                              \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 1, kGlobal, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 1, kSemi, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 1, kLocal, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16};   \
+      }                                                                                            \
+    } else {                                                                                       \
+      switch (mode) {                                                                              \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 2, kGlobal, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 2, kSemi, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 2, kLocal, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16};   \
+      }                                                                                            \
+    }                                                                                              \
+    return {};                                                                                     \
+  }                                                                                                \
   }
 
 #define TA_DEFINE_WAVE_TABLE(G)                                                        \

@@ -226,3 +226,23 @@ def test_wave_pairs_of_different_triplets(gpu_engine, oracle, mode):
         want = oracle.align(t, (1, -1, -2), mode)
         assert int(out["status"][x]) == 0
         assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
+    """Enough long triplets to skip wave mode (> one per two lane streams), with
+    b, c in 150..300: the largest-grid bucket splits into single-block items,
+    160-wide block items and 128-wide block items (8 x 8 tiles, chosen where
+    they pad less, e.g. extents 161..256); every score and end vs the oracle."""
+    rng = np.random.default_rng(500 + mode)
+    trips = []
+    for _ in range(320):
+        a = int(rng.integers(0, 24))
+        b, c = (int(x) for x in rng.integers(150, 301, size=2))
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (a, b, c)))
+    for sch in [(1, -1, -2), (2, -3, -1)]:
+        sc = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.align(t, sch, mode)
+            assert int(sc["status"][x]) == 0
+            assert int(sc["score"][x]) == want["score"] and list(sc["end"][x]) == want["end"], (sch, mode, x)
