@@ -926,9 +926,9 @@ int launch_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int l
 // wider than 80 cells run as block items (faces of 4 values per position).
 
 // Largest biased, gap-shifted value: -8 open + (match - 2 gap) * (slices + extents).
-int64_t aff_lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c) {
+int64_t aff_lane_bound(const ta_scheme& s, int32_t a, int32_t b, int32_t c, int tile_n = ta::kAffN) {
   const int g2 = 2 * s.gap;
-  const int64_t gn = ta::kAffExtent;
+  const int64_t gn = int64_t(ta::kAffG) * tile_n;
   const int64_t ej = ((b + 1 + gn - 1) / gn) * gn, ek = ((c + 1 + gn - 1) / gn) * gn;
   const int warps = (ta::kAffG * ta::kAffG + 31) / 32;
   const int64_t slices = std::max<int64_t>(a + 1, ta::kAffG + 2 + warps);
@@ -942,9 +942,25 @@ bool aff_s16_ok(const ta_scheme& s, int64_t max_bound) {
   return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kAffN + 2 * int64_t(-s.gap_open) <= 32000;
 }
 
+// Block items that pad less in 64-wide blocks (4 x 4 tiles) than in 80-wide
+// ones, weighting a 64-block cell by the per-cell cost ratio of the kernels.
+// Example: 250 bp (extent 251) = 4 x 4 blocks either way: 65536 vs 102400.
+bool prefer_aff4(int32_t b, int32_t c) {
+  static const double ratio = [] {
+    const char* e = std::getenv("TA_AFF4_COST");
+    return e ? std::atof(e) : 1.3;
+  }();
+  const Blocks b5 = blocks_of(b, c, ta::kAffG, ta::kAffN);
+  const Blocks b4 = blocks_of(b, c, ta::kAffG, ta::kAffSmallN);
+  const double g5 = double(ta::kAffG) * ta::kAffN, g4 = double(ta::kAffG) * ta::kAffSmallN;
+  return double(b4.bj * b4.bk) * g4 * g4 * ratio < double(b5.bj * b5.bk) * g5 * g5;
+}
+
 int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mode, bool trace, int blk,
-                cudaStream_t st, BucketLaunch* bl, ta::AffEntry* ae) {
-  *ae = ta::lookup_affine(lanes, mode, trace, blk);
+                cudaStream_t st, BucketLaunch* bl, ta::AffEntry* ae, int tile_n = ta::kAffN) {
+  if (tile_n != ta::kAffN && (blk != 1 || trace))
+    return fail(TA_ERR_LOGIC, "4 x 4 affine tiles exist for block score items only");
+  *ae = tile_n != ta::kAffN ? ta::affine_kernel_blocks4(lanes, mode) : ta::lookup_affine(lanes, mode, trace, blk);
   if (!ae->fn) return fail(TA_ERR_LOGIC, "no affine kernel instantiation");
   TA_CK(cudaFuncSetAttribute(ae->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ae->smem)));
   int per_sm = 0;
@@ -984,7 +1000,7 @@ int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mo
   bl->mode = mode;
   bl->ctas = int(std::max<int64_t>(1, std::min<int64_t>(int64_t(per_sm) * bt->ctx->sms, want)));
   StreamPlan plan;
-  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, ta::kAffG, &plan, ta::kAffN, true);
+  plan_streams(ids, bt->a, bt->b, bt->c, bl->ctas, lanes, ta::kAffG, &plan, tile_n, true);
   if (plan.face_words > (int64_t(1) << 31)) return fail(TA_ERR_CAPACITY, "block-face scratch exceeds 2^31 words");
   TA_CK(bl->items.reserve(plan.items.size()));
   TA_CK(bl->soff.reserve(plan.soff.size()));
@@ -995,7 +1011,7 @@ int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mo
   TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
   TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
-  bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * ta::kAffN * ta::kAffN;
+  bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * tile_n * tile_n;
   return TA_OK;
 }
 
@@ -1047,6 +1063,24 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
     for (int32_t id : multi) ok &= bt->a[size_t(id)] + 1 < 65535;
     if (ok) wave.swap(multi);
   }
+  // block items that pad less in 64-wide blocks (score path), own lane choice
+  std::vector<int32_t> multi4;
+  int lanes4 = 1;
+  if (!rows && !multi.empty()) {
+    std::vector<int32_t> keep;
+    int64_t maxb4 = 0;
+    for (int32_t id : multi) {
+      const int32_t B = bt->b[size_t(id)], C = bt->c[size_t(id)];
+      if (prefer_aff4(B, C)) {
+        multi4.push_back(id);
+        maxb4 = std::max(maxb4, aff_lane_bound(scheme, bt->a[size_t(id)], B, C, ta::kAffSmallN));
+      } else {
+        keep.push_back(id);
+      }
+    }
+    multi.swap(keep);
+    lanes4 = aff_s16_ok(scheme, maxb4) ? 2 : 1;
+  }
   ta::AffArgs base{};
   base.seq = bt->seq.ptr;
   base.desc = bt->d_desc.ptr;
@@ -1078,7 +1112,8 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
   };
   if (!rows) {
     std::string key = "aff:" + std::to_string(opt.mode) + ":" + std::to_string(lanes) + ":" +
-                      std::to_string(scheme.gap_open) + ":" + std::to_string(all_ok.size());
+                      std::to_string(scheme.gap_open) + ":" + std::to_string(all_ok.size()) + ":" +
+                      std::to_string(multi4.size()) + ":" + std::to_string(lanes4);
     uint64_t h = 1469598103934665603ull;
     for (int32_t id : all_ok) h = (h ^ uint64_t(id)) * 1099511628211ull;
     key += ":" + std::to_string(h);
@@ -1086,13 +1121,14 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
       bt->plan_cache.clear();
       bt->aff_cache.clear();
       bt->plan_key.clear();
-      for (int w = 0; w < 3; ++w) {
-        const std::vector<int32_t>& part = w == 2 ? wave : w ? multi : single;
+      for (int w = 0; w < 4; ++w) {
+        const std::vector<int32_t>& part = w == 3 ? multi4 : w == 2 ? wave : w ? multi : single;
         if (part.empty()) continue;
         bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
         bt->aff_cache.emplace_back();
-        if (int rc = aff_prepare(bt, part, lanes, opt.mode, false, w, st, bt->plan_cache.back().get(),
-                                 &bt->aff_cache.back()))
+        if (int rc = aff_prepare(bt, part, w == 3 ? lanes4 : lanes, opt.mode, false, w == 3 ? 1 : w, st,
+                                 bt->plan_cache.back().get(), &bt->aff_cache.back(),
+                                 w == 3 ? ta::kAffSmallN : ta::kAffN))
           return rc;
       }
       bt->plan_key = key;

@@ -10,6 +10,7 @@ namespace ta {
 
 constexpr int kAffG = 16;
 constexpr int kAffExtent = kAffG * kAffN;
+constexpr int kAffSmallN = 4;  // block items in 64-wide blocks (16 x 16 tiles of 4 x 4)
 
 using AffFn = void (*)(AffArgs);
 
@@ -24,6 +25,9 @@ struct AffEntry {
 AffEntry affine_kernel_single(int lanes, int mode, bool trace);
 AffEntry affine_kernel_blocks(int lanes, int mode, bool trace);
 AffEntry affine_kernel_wave(int lanes, int mode, bool trace);
+// 4 x 4 tiles, block items only (no trace): long triplets whose extents pad
+// less in 64-wide blocks than in 80-wide ones
+AffEntry affine_kernel_blocks4(int lanes, int mode);
 
 inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
   if (blk == 2) return trace ? AffEntry{} : affine_kernel_wave(lanes, mode, false);
@@ -63,4 +67,27 @@ inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
     }                                                          \
     return {};                                                 \
   }                                                            \
+  }
+
+#define TA_AFF4_ENTRY(L, M) \
+  AffEntry{&affine_kernel<kAffSmallN, kAffG, L, M, false, 1>, AffSmem<kAffSmallN, kAffG, L, 1>::bytes, kAffG * kAffG}
+
+#define TA_DEFINE_AFF4_TABLE()                          \
+  namespace ta {                                        \
+  AffEntry affine_kernel_blocks4(int lanes, int mode) { \
+    if (lanes == 1) {                                   \
+      switch (mode) {                                   \
+        case kGlobal: return TA_AFF4_ENTRY(1, kGlobal); \
+        case kSemi: return TA_AFF4_ENTRY(1, kSemi);     \
+        case kLocal: return TA_AFF4_ENTRY(1, kLocal);   \
+      }                                                 \
+    } else {                                            \
+      switch (mode) {                                   \
+        case kGlobal: return TA_AFF4_ENTRY(2, kGlobal); \
+        case kSemi: return TA_AFF4_ENTRY(2, kSemi);     \
+        case kLocal: return TA_AFF4_ENTRY(2, kLocal);   \
+      }                                                 \
+    }                                                   \
+    return {};                                          \
+  }                                                     \
   }

@@ -165,3 +165,22 @@ def test_affine_wave_pairs_of_different_triplets(gpu_engine, oracle, mode):
         want = oracle.affine(t, sch, mode)
         assert int(out["status"][x]) == 0
         assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_affine_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
+    """Enough long triplets to skip wave mode, b, c in 70..260: single-block
+    items, 80-wide block items and 64-wide block items (4 x 4 tiles, chosen
+    where they pad less, e.g. extents 81..128 and 193..256) vs the oracle."""
+    rng = np.random.default_rng(600 + mode)
+    trips = []
+    for _ in range(320):
+        a = int(rng.integers(0, 16))
+        b, c = (int(x) for x in rng.integers(70, 261, size=2))
+        trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (a, b, c)))
+    sch = (1, -1, -2, -3)
+    out = run(trips, sch, mode)
+    for x, t in enumerate(trips):
+        want = oracle.affine(t, sch, mode)
+        assert int(out["status"][x]) == 0
+        assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
