@@ -24,7 +24,7 @@ def timed(b, sch, mode, reps=2):
     return best
 
 
-for name, spec, rates, seed, modes, affine in (("C3", "fixed:250:250:250:4000000", (0.025, 0.005), 3, (0,), False),
+for name, spec, rates, seed, modes, affine in (("C3", "fixed:250:250:250:4000000", (0.025, 0.005), 3, (0,), True),
                                                 ("C4", "uniform:64:512:100000", (0.08, 0.01), 4, (0, 1, 2), True)):
     t0 = time.perf_counter()
     seqs, offs = ta.generate(spec, *rates, seed)
