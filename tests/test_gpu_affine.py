@@ -178,9 +178,9 @@ def test_affine_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
         a = int(rng.integers(0, 16))
         b, c = (int(x) for x in rng.integers(70, 261, size=2))
         trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (a, b, c)))
-    sch = (1, -1, -2, -3)
-    out = run(trips, sch, mode)
-    for x, t in enumerate(trips):
-        want = oracle.affine(t, sch, mode)
-        assert int(out["status"][x]) == 0
-        assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (mode, x)
+    for sch in [(1, -1, -2, -3), (50, -50, -30, -40)]:  # the second one needs int32 lanes
+        out = run(trips, sch, mode)
+        for x, t in enumerate(trips):
+            want = oracle.affine(t, sch, mode)
+            assert int(out["status"][x]) == 0
+            assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (sch, mode, x)

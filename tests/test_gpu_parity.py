@@ -240,7 +240,7 @@ def test_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
         a = int(rng.integers(0, 24))
         b, c = (int(x) for x in rng.integers(150, 301, size=2))
         trips.append(tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=L)) for L in (a, b, c)))
-    for sch in [(1, -1, -2), (2, -3, -1)]:
+    for sch in [(1, -1, -2), (2, -3, -1), (100, -100, -50)]:  # the last one needs int32 lanes
         sc = run(trips, sch, mode)
         for x, t in enumerate(trips):
             want = oracle.align(t, sch, mode)
