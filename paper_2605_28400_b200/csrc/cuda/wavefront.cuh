@@ -882,12 +882,24 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           for (int Q = N - 1; Q >= 1; --Q) acc = Ops::addmax(acc, g2s, Cu[P][Q]);
           return acc;
         };
-        // max over P of Cu[P][Q] + g2 * (P - 1)
-        auto col_max = [&](int Q) -> uint32_t {
-          uint32_t acc = Cu[N][Q];
+        // fr[Q - 1] = Cu[p + 1][Q] / fc[P - 1] = Cu[P][q + 1] for a run-time p / q in [0, N)
+        auto select_row = [&](int p, uint32_t (&fr)[N]) {
 #pragma unroll
-          for (int P = N - 1; P >= 1; --P) acc = Ops::addmax(acc, g2s, Cu[P][Q]);
-          return acc;
+          for (int Q = 1; Q <= N; ++Q) {
+            uint32_t v = Cu[1][Q];
+#pragma unroll
+            for (int P = 2; P <= N; ++P) v = p == P - 1 ? Cu[P][Q] : v;
+            fr[Q - 1] = v;
+          }
+        };
+        auto select_col = [&](int q, uint32_t (&fc)[N]) {
+#pragma unroll
+          for (int P = 1; P <= N; ++P) {
+            uint32_t v = Cu[P][1];
+#pragma unroll
+            for (int Q = 2; Q <= N; ++Q) v = q == Q - 1 ? Cu[P][Q] : v;
+            fc[P - 1] = v;
+          }
         };
         if (anyfull) {
           uint32_t stepmax = row_max(N);
@@ -899,20 +911,20 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             const int sm = Ops::lane(stepmax, l);  // scaled by SC, relative to the tile origin
             const int mval = (sm >> SH) + g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
             if (may_beat(l, mval)) {
-              // first row, then first cell of that row, attaining the maximum
+              // first row, then first cell of that row, attaining the maximum;
+              // the row is selected into fr (one SEL per cell) so the scan
+              // below exists once, not once per row (code size: the semi /
+              // local loops were instruction-cache bound)
               int fp = 0;
 #pragma unroll
               for (int P = N; P >= 1; --P)
                 if (Ops::lane(row_max(P), l) + g2 * SC * (P - 1) == sm) fp = P;
+              uint32_t fr[N];
+              select_row(fp - 1, fr);
               int fq = 0;
 #pragma unroll
-              for (int P = 1; P <= N; ++P) {
-                if (P == fp) {
-#pragma unroll
-                  for (int Q = N; Q >= 1; --Q)
-                    if (Ops::lane(Cu[P][Q], l) + g2 * SC * (P - 1 + Q - 1) == sm) fq = Q;
-                }
-              }
+              for (int Q = N; Q >= 1; --Q)
+                if (Ops::lane(fr[Q - 1], l) + g2 * SC * (fp - 1 + Q - 1) == sm) fq = Q;
               offer(l, mval, fp, fq);
             }
           }
@@ -924,43 +936,42 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             for (int l = 0; l < LANES; ++l) {
               if (!face[l]) continue;
               const int base = g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
+              const int rbl = rb[l], cbl = cb[l];
+              const bool hasr = rbl < N, hasc = cbl < N;
+              // the face row (P = rb + 1) and column (Q = cb + 1) of the tile
+              uint32_t fr[N], fc[N];
+              select_row(rbl, fr);
+              select_col(cbl, fc);
               int fm = INT_MIN;
-              if (rb[l] < N) {
+              if (hasr) {
+                uint32_t acc = fr[N - 1];
 #pragma unroll
-                for (int P = 1; P <= N; ++P)
-                  if (P - 1 == rb[l]) fm = (Ops::lane(row_max(P), l) >> SH) + g2 * (P - 1);
+                for (int Q = N - 1; Q >= 1; --Q) acc = Ops::addmax(acc, g2s, fr[Q - 1]);
+                fm = (Ops::lane(acc, l) >> SH) + g2 * rbl;
               }
-              if (cb[l] < N) {
+              if (hasc) {
+                uint32_t acc = fc[N - 1];
 #pragma unroll
-                for (int Q = 1; Q <= N; ++Q)
-                  if (Q - 1 == cb[l]) fm = max(fm, (Ops::lane(col_max(Q), l) >> SH) + g2 * (Q - 1));
+                for (int P = N - 1; P >= 1; --P) acc = Ops::addmax(acc, g2s, fc[P - 1]);
+                fm = max(fm, (Ops::lane(acc, l) >> SH) + g2 * cbl);
               }
               if (!may_beat(l, fm + base)) continue;
               int bv = 0, bp = 0, bq = 0;
               bool have = false;
-              if (rb[l] < N) {
-#pragma unroll
-                for (int P = 1; P <= N; ++P) {
-                  if (P - 1 == rb[l]) {
-#pragma unroll
-                    for (int Q = 1; Q <= N; ++Q) {
-                      const int v = (Ops::lane(Cu[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1);
-                      if (!have || v > bv) bv = v, bp = P, bq = Q, have = true;
-                    }
-                  }
-                }
-              }
-              if (cb[l] < N) {
+              if (hasr) {
 #pragma unroll
                 for (int Q = 1; Q <= N; ++Q) {
-                  if (Q - 1 == cb[l]) {
+                  const int v = (Ops::lane(fr[Q - 1], l) >> SH) + g2 * (rbl + Q - 1);
+                  if (!have || v > bv) bv = v, bq = Q, have = true;
+                }
+                bp = rbl + 1;
+              }
+              if (hasc) {
 #pragma unroll
-                    for (int P = 1; P <= N; ++P) {
-                      const int v = (Ops::lane(Cu[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1);
-                      // row-major order between the two faces: smaller P first
-                      if (!have || v > bv || (v == bv && P < bp)) bv = v, bp = P, bq = Q, have = true;
-                    }
-                  }
+                for (int P = 1; P <= N; ++P) {
+                  const int v = (Ops::lane(fc[P - 1], l) >> SH) + g2 * (P - 1 + cbl);
+                  // row-major order between the two faces: smaller P first
+                  if (!have || v > bv || (v == bv && P < bp)) bv = v, bp = P, bq = cbl + 1, have = true;
                 }
               }
               offer(l, bv + base, bp, bq);
