@@ -734,18 +734,39 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             for (int l = 0; l < LANES; ++l) {
               if (!face[l]) continue;
               const int base = -args.bias + g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
+              const int rbl = rb[l], cbl = cb[l];
+              // the face row (P = rb + 1, real cells Q - 1 <= cb) and column
+              // (Q = cb + 1, P - 1 <= rb), selected with SEL chains and scanned
+              // once: row first, then the column cells that come earlier in
+              // row-major order win ties
+              uint32_t fr[N], fc[N];
+#pragma unroll
+              for (int x = 1; x <= N; ++x) {
+                uint32_t vr = cB[1][x], vc = cB[x][1];
+#pragma unroll
+                for (int y = 2; y <= N; ++y) {
+                  vr = rbl == y - 1 ? cB[y][x] : vr;
+                  vc = cbl == y - 1 ? cB[x][y] : vc;
+                }
+                fr[x - 1] = vr;
+                fc[x - 1] = vc;
+              }
               int bv = 0, bp = 0, bq = 0;
               bool have = false;
-#pragma unroll
-              for (int P = 1; P <= N; ++P)
+              if (rbl < N) {
 #pragma unroll
                 for (int Q = 1; Q <= N; ++Q) {
-                  const bool on = (P - 1 == rb[l] && Q - 1 <= cb[l]) || (Q - 1 == cb[l] && P - 1 <= rb[l]);
-                  if (on) {
-                    const int v = (Ops::lane(cB[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1);
-                    if (!have || v > bv) bv = v, bp = P, bq = Q, have = true;
-                  }
+                  const int v = (Ops::lane(fr[Q - 1], l) >> SH) + g2 * (rbl + Q - 1);
+                  if (Q - 1 <= cbl && (!have || v > bv)) bv = v, bp = rbl + 1, bq = Q, have = true;
                 }
+              }
+              if (cbl < N) {
+#pragma unroll
+                for (int P = 1; P <= N; ++P) {
+                  const int v = (Ops::lane(fc[P - 1], l) >> SH) + g2 * (P - 1 + cbl);
+                  if (P - 1 <= rbl && (!have || v > bv || (v == bv && P < bp))) bv = v, bp = P, bq = cbl + 1, have = true;
+                }
+              }
               if (have && may_beat(l, bv + base)) offer(l, bv + base, bp, bq);
             }
           }
