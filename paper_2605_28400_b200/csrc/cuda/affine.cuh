@@ -703,12 +703,13 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           return lop_sel(NEG, cB[P][Q], m);
         };
         if (anyfull) {
-          uint32_t stepmax = NEG;
+          uint32_t stepmax = NEG, rowacc[N];
 #pragma unroll
           for (int P = N; P >= 1; --P) {
             uint32_t acc = cellv(P, N);
 #pragma unroll
             for (int Q = N - 1; Q >= 1; --Q) acc = Ops::addmax(acc, g2s, cellv(P, Q));
+            rowacc[P - 1] = acc;
             stepmax = P == N ? acc : Ops::addmax(stepmax, g2s, acc);
           }
 #pragma unroll
@@ -717,13 +718,20 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             const int sm = Ops::lane(stepmax, l) >> SH;
             const int mval = sm - args.bias + g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
             if (may_beat(l, mval)) {
-              int fp = 0, fq = 0;
+              // first row attaining the maximum (its masked row max), then the
+              // first real cell of that row (selected with a SEL chain)
+              int fp = 0;
 #pragma unroll
               for (int P = N; P >= 1; --P)
+                if ((Ops::lane(rowacc[P - 1], l) >> SH) + g2 * (P - 1) == sm) fp = P;
+              int fq = 0;
 #pragma unroll
-                for (int Q = N; Q >= 1; --Q)
-                  if (P - 1 <= rb[l] && Q - 1 <= cb[l] && (Ops::lane(cB[P][Q], l) >> SH) + g2 * (P - 1 + Q - 1) == sm)
-                    fp = P, fq = Q;
+              for (int Q = N; Q >= 1; --Q) {
+                uint32_t v = cB[1][Q];
+#pragma unroll
+                for (int P = 2; P <= N; ++P) v = fp == P ? cB[P][Q] : v;
+                if (Q - 1 <= cb[l] && (Ops::lane(v, l) >> SH) + g2 * (fp - 1 + Q - 1) == sm) fq = Q;
+              }
               offer(l, mval, fp, fq);
             }
           }
