@@ -940,8 +940,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               const bool hasr = rbl < N, hasc = cbl < N;
               // the face row (P = rb + 1) and column (Q = cb + 1) of the tile
               uint32_t fr[N], fc[N];
-              select_row(rbl, fr);
-              select_col(cbl, fc);
+              if (hasr) select_row(rbl, fr);
+              if (hasc) select_col(cbl, fc);
               int fm = INT_MIN;
               if (hasr) {
                 uint32_t acc = fr[N - 1];
