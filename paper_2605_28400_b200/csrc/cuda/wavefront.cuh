@@ -872,8 +872,16 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               &bkey[l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1))]);
           return key_of(mval, lin_of(l, 1, 1)) > cur;
         };
+        // The offer is a fire-and-forget 64-bit max in global memory (native
+        // RED.MAX.64; a 64-bit shared-memory atomicMax is a CAS spin loop that
+        // the face threads of a step contend on).  The shared slot keeps only a
+        // filter hint: a plain store of an offered key, so it never exceeds
+        // the true best (a racing lower store only lets later offers through).
         auto offer = [&](int l, int mval, int P, int Q) {
-          atomicMax(&bkey[l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1))], key_of(mval, lin_of(l, P, Q)));
+          const unsigned long long key = key_of(mval, lin_of(l, P, Q));
+          atomicMax(args.out_key + LS(l, kTid), key);
+          volatile unsigned long long* hint = &bkey[l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1))];
+          if (key > *hint) *hint = key;
         };
         // max over Q of Cu[P][Q] + g2 * (Q - 1) (Horner, one VIADDMNMX per cell)
         auto row_max = [&](int P) -> uint32_t {
