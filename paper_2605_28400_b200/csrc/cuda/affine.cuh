@@ -690,7 +690,13 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           const unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&bkey[slot_of(l)]);
           return key_of(mval, lin_of(l, 1, 1)) > cur;
         };
-        auto offer = [&](int l, int mval, int P, int Q) { atomicMax(&bkey[slot_of(l)], key_of(mval, lin_of(l, P, Q))); };
+        // global RED.MAX.64 + shared filter hint (see wavefront.cuh)
+        auto offer = [&](int l, int mval, int P, int Q) {
+          const unsigned long long key = key_of(mval, lin_of(l, P, Q));
+          atomicMax(args.out_key + LS(l, kTid), key);
+          volatile unsigned long long* hint = &bkey[slot_of(l)];
+          if (key > *hint) *hint = key;
+        };
         // value of cell (P, Q) for the scans: padding masked to NEG
         auto cellv = [&](int P, int Q) -> uint32_t {
           uint32_t m = 0xFFFFFFFFu;
