@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Small batches through every kernel family, for compute-sanitizer
 (memcheck / racecheck / synccheck): linear score + rows in all modes, a long
-(multi-block) and a wave-mode triplet set, affine score + rows."""
+(multi-block) and a wave-mode triplet set, affine score + rows, and enough
+long triplets to skip wave mode (the 128-wide linear / 64-wide affine block
+items)."""
 import os
 import sys
 
@@ -30,10 +32,13 @@ def arrays(ts):
 
 small = arrays(trips(40, 0, 60))
 long_ = arrays(trips(3, 165, 330))
+many = [tuple("".join("ACGT"[x] for x in rng.integers(0, 4, size=int(L))) for L in (int(rng.integers(0, 4)), b, c))
+        for b, c in rng.integers(165, 256, size=(160, 2))]
+many = arrays(many)
 for mode in (0, 1, 2):
     m = ta.AlignmentMode(mode)
     for sch in (ta.ScoringScheme(1, -1, -2), ta.ScoringScheme(1, -1, -2, -3)):
-        for seqs, offs in (small, long_):
+        for seqs, offs in (small, long_, many):
             ta.align_arrays(seqs, offs, sch, m, cfg=ta.EngineConfig(cell_budget=1 << 40))
         ta.align_arrays(*small, sch, m, with_rows=True, cell_budget=1 << 40)
 print("sanitize workload done")
