@@ -626,7 +626,11 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       // ---- 3. forced cells (reference initialisation, oracle.cpp:30-39) --
       // global: M(0,0,0) = 0; semi: axis cells are 0 in M-space.
       uint32_t fcorner = NEG;
-      uint32_t frow[MODE == kSemi ? N : 1], fcol[MODE == kSemi ? N : 1];
+      // semi slice-0 axis cells: row P = 1 / column Q = 1 start values as a
+      // packed base plus a per-cell step (NEG base and 0 step in lanes that
+      // force nothing), folded into the one sweep (no second copy of the tile
+      // loop: the semi kernel was instruction-cache bound)
+      uint32_t frb = NEG, fcb = NEG, frs = 0u, fcs = 0u;
       uint32_t flbase = 0;
       bool force = false;  // semi: this step computes slice-0 axis cells of a lane
       if constexpr (MODE == kSemi) {
@@ -635,10 +639,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
           force |= !(flags[l] & kDone) && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0));
         }
-      }
-      if (force) {
-#pragma unroll
-        for (int q = 0; q < N; ++q) frow[q] = fcol[q] = NEG;
       }
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
@@ -650,11 +650,14 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
           if (t == 0 && live && oj == 0 && ok == 0 && si[l] <= la[l])
             fcorner = lop_sel(fcorner, Ops::splat((ag2 * si[l]) << SH), Ops::mask(l));
-          if (force && live && si[l] == 0 && ((r == 0 && oj == 0) || (cc == 0 && ok == 0))) {
-#pragma unroll
-            for (int q = 0; q < N; ++q) {
-              if (r == 0 && oj == 0) frow[q] = lop_sel(frow[q], Ops::splat((ag2 * (ok + k0 + q)) << SH), Ops::mask(l));
-              if (cc == 0 && ok == 0) fcol[q] = lop_sel(fcol[q], Ops::splat((ag2 * (oj + j0 + q)) << SH), Ops::mask(l));
+          if (force && live && si[l] == 0) {
+            if (r == 0 && oj == 0) {
+              frb = lop_sel(frb, Ops::splat((ag2 * (ok + k0)) << SH), Ops::mask(l));
+              frs = lop_sel(frs, Ops::splat(ag2 << SH), Ops::mask(l));
+            }
+            if (cc == 0 && ok == 0) {
+              fcb = lop_sel(fcb, Ops::splat((ag2 * (oj + j0)) << SH), Ops::mask(l));
+              fcs = lop_sel(fcs, Ops::splat(ag2 << SH), Ops::mask(l));
             }
           }
         } else {
@@ -673,10 +676,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       // row on the FMA pipe (values >= 0: packed adds never carry)
       const uint32_t ag2s = Ops::splat(ag2 * (1 << SH));
       uint32_t flrow = flbase + (TRACE ? kTagStop : 0u);
-      // The slice-0 axis cells of semi-global mode are forced in a separate
-      // instance of the tile loop, so ordinary steps carry no forcing maxima.
-      auto sweep_tile = [&](auto force_tag) {
-      constexpr bool FORCE = decltype(force_tag)::value;
+      auto sweep_tile = [&]() {
       // Cells in anti-diagonal order (d = P + Q): consecutive cells are
       // independent, so the row / column dependencies of the recurrence are
       // ~N instructions apart instead of back to back.  sigma12' is stored in
@@ -689,6 +689,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       }
       uint4 sg4 = make_uint4(0, 0, 0, 0);
       [[maybe_unused]] uint32_t fd = flrow;  // local floor of diagonal d (depends on P + Q only)
+      [[maybe_unused]] uint32_t frv = frb, fcv = fcb;  // semi: start of the next row-1 / column-1 cell
       int k = 0;
 #pragma unroll
       for (int d = 0; d <= 2 * N - 2; ++d) {
@@ -728,9 +729,16 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           if constexpr (MODE == kGlobal || MODE == kSemi) {
             if (P == 1 && Q == 1) x = Ops::max2(x, fcorner);
           }
-          if constexpr (MODE == kSemi && FORCE) {
-            if (P == 1) x = Ops::max2(x, frow[Q - 1]);
-            if (Q == 1) x = Ops::max2(x, fcol[P - 1]);
+          if constexpr (MODE == kSemi) {
+            // row-1 cells are visited with Q increasing, column-1 cells with P
+            if (P == 1) {
+              x = Ops::max2(x, frv);
+              if (Q < N) frv = fma_add(frv, one, frs);
+            }
+            if (Q == 1) {
+              x = Ops::max2(x, fcv);
+              if (P < N) fcv = fma_add(fcv, one, fcs);
+            }
           }
           if constexpr (TRACE) {
             dirw[cell >> 3] |= (x & 15u) << ((cell & 7) * 4);
@@ -740,11 +748,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
       }
       };
-      if (MODE == kSemi && force) {
-        sweep_tile(std::true_type{});
-      } else {
-        sweep_tile(std::false_type{});
-      }
+      sweep_tile();
 
       // ---- 5. publish right column / down row (+ corner) ----------------
       uint32_t* xout = xbuf + buf * XW * (T + 1) + tile;
