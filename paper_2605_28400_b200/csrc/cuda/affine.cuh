@@ -439,7 +439,10 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       uint32_t stbase = NEG;  // local: start value of the tile's cell (1, 1)
       uint32_t fcorner = NEG;
       bool force = false;
-      uint32_t frow[MODE == kSemi ? N : 1], fcol[MODE == kSemi ? N : 1];
+      // semi slice-0 axis starts of row P = 1 / column Q = 1: packed base +
+      // per-cell step (NEG / 0 in lanes that force nothing), folded into the
+      // one sweep (see wavefront.cuh)
+      uint32_t frb = NEG, fcb = NEG, frs = 0u, fcs = 0u;
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
         const bool live = !(flags[l] & kDone);
@@ -459,17 +462,16 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       if constexpr (MODE == kSemi) {
         if (force) {
 #pragma unroll
-          for (int q = 0; q < N; ++q) frow[q] = fcol[q] = NEG;
-#pragma unroll
           for (int l = 0; l < LANES; ++l) {
             const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
             if ((flags[l] & kDone) || si[l] != 0) continue;
-#pragma unroll
-            for (int q = 0; q < N; ++q) {
-              if (r == 0 && oj == 0)
-                frow[q] = lop_sel(frow[q], Ops::splat((args.bias + ag2 * (ok + k0 + q)) * SC + (SC - 1)), Ops::mask(l));
-              if (cc == 0 && ok == 0)
-                fcol[q] = lop_sel(fcol[q], Ops::splat((args.bias + ag2 * (oj + j0 + q)) * SC + (SC - 1)), Ops::mask(l));
+            if (r == 0 && oj == 0) {
+              frb = lop_sel(frb, Ops::splat((args.bias + ag2 * (ok + k0)) * SC + (SC - 1)), Ops::mask(l));
+              frs = lop_sel(frs, Ops::splat(ag2 * SC), Ops::mask(l));
+            }
+            if (cc == 0 && ok == 0) {
+              fcb = lop_sel(fcb, Ops::splat((args.bias + ag2 * (oj + j0)) * SC + (SC - 1)), Ops::mask(l));
+              fcs = lop_sel(fcs, Ops::splat(ag2 * SC), Ops::mask(l));
             }
           }
         }
@@ -477,9 +479,9 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       const uint32_t ag2s = Ops::splat(ag2 * SC);
 
       // ---- 4. the tile -------------------------------------------------------
-      auto sweep = [&](auto force_tag) {
-        [[maybe_unused]] constexpr bool FORCE = decltype(force_tag)::value;
+      auto sweep = [&]() {
         uint32_t strow = stbase;
+        [[maybe_unused]] uint32_t frv = frb, fcv = fcb;
 #pragma unroll
         for (int P = 1; P <= N; ++P) {
           const uint32_t a1 = sig_row(tab1, P - 1);
@@ -499,9 +501,15 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               if (Q < N) st = fma_add(st, one, ag2s);
             } else {
               if (P == 1 && Q == 1) start = fcorner;
-              if constexpr (MODE == kSemi && FORCE) {
-                if (P == 1) start = Ops::max2(start, frow[Q - 1]);
-                if (Q == 1) start = Ops::max2(start, fcol[P - 1]);
+              if constexpr (MODE == kSemi) {
+                if (P == 1) {
+                  start = Ops::max2(start, frv);
+                  if (Q < N) frv = fma_add(frv, one, frs);
+                }
+                if (Q == 1) {
+                  start = Ops::max2(start, fcv);
+                  if (P < N) fcv = fma_add(fcv, one, fcs);
+                }
               }
             }
             const uint32_t y = fma_add(fma_add(pB[P - 1][Q - 1], one, a1), one, a2);
@@ -540,11 +548,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           }
         }
       };
-      if (MODE == kSemi && force) {
-        sweep(std::true_type{});
-      } else {
-        sweep(std::false_type{});
-      }
+      sweep();
 
       // ---- 5. publish right column / bottom row -----------------------------
       uint32_t* xout = xbuf + buf * XW * (T + 1) + tile;
