@@ -6,6 +6,8 @@
 #pragma once
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <exception>
 #include <functional>
 #include <sstream>
@@ -99,7 +101,21 @@ inline void fail(const char* file, int line, const char* expr, bool fatal) {
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main() {
   long cases_failed = 0;
+  // DOCTEST_ONLY="prefix1|prefix2": run only the cases whose name starts with one
+  const char* only = std::getenv("DOCTEST_ONLY");
+  size_t ran = 0;
   for (const auto& c : ::doctest::detail::registry()) {
+    if (only && *only) {
+      bool hit = false;
+      for (const char* p = only; *p;) {
+        const char* e = std::strchr(p, '|');
+        const size_t n = e ? size_t(e - p) : std::strlen(p);
+        hit |= std::strncmp(c.name, p, n) == 0;
+        p += n + (e ? 1 : 0);
+      }
+      if (!hit) continue;
+    }
+    ++ran;
     const long before = ::doctest::detail::failures();
     try {
       c.fn();
@@ -112,8 +128,7 @@ int main() {
       std::fprintf(stderr, "case FAILED: %s\n", c.name);
     }
   }
-  std::printf("[doctest-shim] test cases: %zu | %ld failed | checks: %ld | %ld failed\n",
-              ::doctest::detail::registry().size(), cases_failed, ::doctest::detail::checks(),
+  std::printf("[doctest-shim] test cases: %zu | %ld failed | checks: %ld | %ld failed\n", ran, cases_failed, ::doctest::detail::checks(),
               ::doctest::detail::failures());
   return cases_failed == 0 ? 0 : 1;
 }

@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
                 uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kAffSegE + e];
                 while (v.y != want) {
-                  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(src + e));
+                  v = ld_face(src + e);
                 }
                 return static_cast<int32_t>(v.x);
               };
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             const uint32_t tag = (static_cast<uint32_t>(args.epoch) << 16) + static_cast<uint32_t>(si[l]) + 1u;
             uint2* fb = reinterpret_cast<uint2*>(reinterpret_cast<uint64_t*>(args.faces) + args.face_off[LS(l, kTid)]);
             const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
-            auto put = [&](uint2* d, int e, uint32_t v) { d[e] = make_uint2(static_cast<uint32_t>(Ops::lane(v, l)), tag); };
+            auto put = [&](uint2* d, int e, uint32_t v) { st_face(d + e, static_cast<uint32_t>(Ops::lane(v, l)), tag); };
             if (dn) {  // segment cc: q = 0 is the corner (this tile's halo), q = 1..N its bottom row
               uint2* d = fb + ((int64_t(blk) * 2 * a1 + si[l]) * G + cc) * kAffSegE;
               put(d, 0, cB[N][0]);
@@ -680,13 +680,10 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           anyface |= face[l];
           edge |= full[l] && (rb[l] < N - 1 || cb[l] < N - 1);
         }
-        auto key_of = [](int mval, uint32_t lin) -> unsigned long long {
-          return (static_cast<unsigned long long>(static_cast<uint32_t>(mval) ^ 0x80000000u) << 32) |
-                 static_cast<unsigned long long>(0xFFFFFFFFu - lin);
-        };
-        auto lin_of = [&](int l, int P, int Q) -> uint32_t {
+        auto key_of = [](int mval, unsigned long long lin) -> unsigned long long { return best_key(mval, lin); };
+        auto lin_of = [&](int l, int P, int Q) -> unsigned long long {
           const uint32_t j = LS(l, kOrgJ) + j0 + P - 1, k = LS(l, kOrgK) + k0 + Q - 1;
-          return (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
+          return (static_cast<unsigned long long>(static_cast<uint32_t>(si[l])) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
                      static_cast<uint32_t>(LS(l, kLenC) + 1) + k;
         };
         auto slot_of = [&](int l) { return l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1)); };

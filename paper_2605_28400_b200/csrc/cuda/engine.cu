@@ -134,13 +134,13 @@ __global__ void decode_keys_kernel(const unsigned long long* __restrict__ key,
   const int32_t id = ids[x];
   const unsigned long long k = key[id];
   const ta::TripletDesc d = desc[id];
-  const uint32_t lin = 0xFFFFFFFFu - static_cast<uint32_t>(k & 0xFFFFFFFFull);
-  const uint32_t plane = static_cast<uint32_t>(d.b + 1) * static_cast<uint32_t>(d.c + 1);
-  const uint32_t i = lin / plane;
-  const uint32_t rem = lin - i * plane;
-  const uint32_t j = rem / static_cast<uint32_t>(d.c + 1);
-  const uint32_t kk = rem - j * static_cast<uint32_t>(d.c + 1);
-  score[id] = static_cast<int32_t>(static_cast<uint32_t>(k >> 32) ^ 0x80000000u);
+  const unsigned long long lin = ta::key_lin(k);
+  const unsigned long long plane = static_cast<unsigned long long>(d.b + 1) * static_cast<unsigned long long>(d.c + 1);
+  const unsigned long long i = lin / plane;
+  const unsigned long long rem = lin - i * plane;
+  const unsigned long long j = rem / static_cast<unsigned long long>(d.c + 1);
+  const unsigned long long kk = rem - j * static_cast<unsigned long long>(d.c + 1);
+  score[id] = ta::key_value(k);
   end[3 * id] = static_cast<int32_t>(i);
   end[3 * id + 1] = static_cast<int32_t>(j);
   end[3 * id + 2] = static_cast<int32_t>(kk);
@@ -466,6 +466,19 @@ bool s16_ok(const ta_scheme& s, int64_t max_bound) {
   if (mm < 0 || mp > 127) return false;  // carry-free packed adds + byte tables
   // values in [0, bound]; unreachable terms stay below 0 from NEG = -16384
   return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kTileN <= 32000;
+}
+
+// Semi-global / local best-cell keys (ta::best_key) hold 36 bits of cell
+// index and 28 bits of biased value: the triplet's tensor must have at most
+// 2^36 cells and every value must stay within +-2^27 (|M| <= (a+b+c) times
+// the largest per-column score, packed_score_bound's argument, plus opening
+// penalties for affine gaps).
+bool key_fits(int32_t a, int32_t b, int32_t c, const ta_scheme& s) {
+  const uint64_t cells = uint64_t(a + 1) * uint64_t(b + 1) * uint64_t(c + 1);
+  if (cells > (uint64_t(1) << ta::kKeyLinBits)) return false;
+  const int64_t per = 3 * (std::max({std::abs(int64_t(s.match)), std::abs(int64_t(s.mismatch)),
+                                     std::abs(int64_t(s.gap))}) + std::abs(int64_t(s.gap_open)));
+  return (int64_t(a) + b + c + 1) * per < (int64_t(1) << 27) - 4096;
 }
 
 // Smallest tile grid whose plane holds the triplet; longer triplets use the
@@ -891,8 +904,12 @@ int launch_prepared(BucketLaunch* bl, const ta::WaveArgs& base, cudaStream_t st,
       ta::WaveArgs ra = args;
       ra.stream_off = bl->soff.ptr + rd.soff_at;
       ra.cta_steps = bl->steps.ptr + rd.steps_at;
-      bl->ke.fn<<<rd.ctas, bl->ke.threads, bl->ke.smem, st>>>(ra);
-      TA_CK(cudaGetLastError());
+      // CTAs of a wave round wait on each other's faces: the cooperative
+      // launch guarantees they are co-resident (or fails loudly), whatever
+      // else runs on the device
+      void* kargs[] = {&ra};
+      TA_CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(bl->ke.fn), dim3(rd.ctas), dim3(bl->ke.threads),
+                                        kargs, bl->ke.smem, st));
       *launches += 1;
     }
     return TA_OK;
@@ -1034,8 +1051,9 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
       ta::AffArgs ra = args;
       ra.stream_off = bl->soff.ptr + rd.soff_at;
       ra.cta_steps = bl->steps.ptr + rd.steps_at;
-      ae.fn<<<rd.ctas, ae.threads, ae.smem, st>>>(ra);
-      TA_CK(cudaGetLastError());
+      void* kargs[] = {&ra};  // co-resident CTAs (see launch_prepared)
+      TA_CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ae.fn), dim3(rd.ctas), dim3(ae.threads), kargs,
+                                        ae.smem, st));
       *launches += 1;
     }
     return TA_OK;
@@ -1264,8 +1282,8 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
         continue;
       }
     }
-    if (opt.mode != TA_GLOBAL && uint64_t(A + 1) * uint64_t(B + 1) * uint64_t(C + 1) > 0xFFFFFFFFull) {
-      bt->status[size_t(t)] = TA_ERR_CAPACITY;  // lexicographic key needs < 2^32 cells
+    if (opt.mode != TA_GLOBAL && !key_fits(A, B, C, scheme)) {
+      bt->status[size_t(t)] = TA_ERR_CAPACITY;
       continue;
     }
     const int g = pick_grid(B, C);
@@ -1538,8 +1556,7 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
       status[t] = TA_ERR_CONFIG;
       continue;
     }
-    if (opt.mode != TA_GLOBAL && uint64_t(a[t] + 1) * uint64_t(b[t] + 1) * uint64_t(c[t] + 1) > 0xFFFFFFFFull)
-      status[t] = TA_ERR_CAPACITY;  // lexicographic key needs < 2^32 cells
+    if (opt.mode != TA_GLOBAL && !key_fits(a[t], b[t], c[t], scheme)) status[t] = TA_ERR_CAPACITY;
   }
   TA_CK(ctx->d_words.reserve(size_t(words) + 2));
   TA_CK(ctx->d_desc.reserve(nn));
@@ -1846,6 +1863,7 @@ int ta_batch_run(ta_batch* b, const ta_scheme* scheme, const ta_options* opt, vo
     // rows need the row buffers; use ta_align_batch for the rows path
     return fail(TA_ERR_INVALID_ARGUMENT, "ta_batch_run computes scores; rows go through ta_align_batch");
   }
+  std::lock_guard<std::mutex> lock(b->ctx->mu);  // one engine run per device at a time
   return run_impl(b, *scheme, *opt, st, nullptr);
 }
 

@@ -46,6 +46,26 @@ constexpr int kLocal = 2;
 constexpr uint32_t kTagT1 = 12, kTagT2 = 5, kTagT3 = 4, kTagT4 = 3;
 constexpr uint32_t kTagT5 = 2, kTagT6 = 1, kTagT7 = 0, kTagStop = 15;
 
+// Semi-global / local best-cell key (optimal_score, oracle.cpp:67-88): one
+// 64-bit word that orders by larger value, then smaller lexicographic (i, j, k)
+// = smaller linear index lin = (i (b+1) + j)(c+1) + k.  28 bits of biased
+// value above 36 bits of ~lin, so triplets of up to 2^36 cells (a 2000 bp
+// triplet has 8e9 > 2^32) keep exact tie-breaks; the host rejects a triplet
+// whose cell count or score bound does not fit (CapacityError).  Key 0 = none.
+constexpr int kKeyLinBits = 36;
+constexpr unsigned long long kKeyLinMask = (1ull << kKeyLinBits) - 1ull;
+constexpr int kKeyValBias = 1 << 27;
+__host__ __device__ __forceinline__ unsigned long long best_key(int mval, unsigned long long lin) {
+  return (static_cast<unsigned long long>(static_cast<uint32_t>(mval + kKeyValBias)) << kKeyLinBits) |
+         (kKeyLinMask - lin);
+}
+__host__ __device__ __forceinline__ int key_value(unsigned long long key) {
+  return static_cast<int>(static_cast<uint32_t>(key >> kKeyLinBits)) - kKeyValBias;
+}
+__host__ __device__ __forceinline__ unsigned long long key_lin(unsigned long long key) {
+  return kKeyLinMask - (key & kKeyLinMask);
+}
+
 struct TripletDesc {
   int32_t a, b, c, flags;
   uint32_t w0, w1, w2, pad;  // word offsets of s0/s1/s2 in the packed array
@@ -183,6 +203,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// Wave-mode face entries: (value, tag) as ONE 64-bit word, published and
+// re-read with single-copy-atomic relaxed gpu-scope accesses, so a consumer
+// that sees the new tag also sees the new value (PTX memory model).
+__device__ __forceinline__ void st_face(void* p, uint32_t value, uint32_t tag) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p),
+               "l"((static_cast<unsigned long long>(tag) << 32) | value)
+               : "memory");
+}
+__device__ __forceinline__ uint2 ld_face(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+}
+
 __device__ __forceinline__ uint32_t lop_sel(uint32_t a, uint32_t b, uint32_t m) {
   return (a & ~m) | (b & m);  // one LOP3
 }
@@ -249,7 +283,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   int32_t* const stage = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX + SM::kLane);  // [LANES][2G][N+1]
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(tab2 + SM::kTab + SM::kX + SM::kLane + SM::kStage);
   // Best (value, cell) of every open stream item, shared by the CTA's threads:
-  // key = (value ^ 2^31) << 32 | ~lin (larger value, then smaller (i, j, k));
+  // key = best_key(value, lin) (larger value, then smaller (i, j, k));
   // bcnt counts threads that finished the item (the last one flushes).
   unsigned long long* const bkey = reinterpret_cast<unsigned long long*>(mbar + 2);     // [LANES][kSlots]
   uint32_t* const bcnt = reinterpret_cast<uint32_t*>(bkey + LANES * SM::kSlots);         // [LANES][kSlots]
@@ -560,7 +594,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
                 uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kSegE + e];
                 while (v.y != want) {
-                  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(src + e));
+                  v = ld_face(src + e);
                 }
                 return static_cast<int32_t>(v.x);
               };
@@ -772,12 +806,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             if (dn) {  // down ring of this block: segment cc, entries q = 0..N (q = 0 is the corner)
               uint2* d = reinterpret_cast<uint2*>(fb + ((int64_t(blk) * 2 * a1 + si[l]) * G + cc) * kSegE);
 #pragma unroll
-              for (int q = 0; q <= N; ++q) d[q] = make_uint2(static_cast<uint32_t>(Ops::lane(Cu[N][q], l) >> SH), tag);
+              for (int q = 0; q <= N; ++q) st_face(d + q, static_cast<uint32_t>(Ops::lane(Cu[N][q], l) >> SH), tag);
             }
             if (rt) {  // right ring: segment r, entries p = 0..N-1
               uint2* d = reinterpret_cast<uint2*>(fb + (((int64_t(blk) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
 #pragma unroll
-              for (int p = 0; p < N; ++p) d[p] = make_uint2(static_cast<uint32_t>(Ops::lane(Cu[p + 1][N], l) >> SH), tag);
+              for (int p = 0; p < N; ++p) st_face(d + p, static_cast<uint32_t>(Ops::lane(Cu[p + 1][N], l) >> SH), tag);
             }
             continue;
           }
@@ -860,13 +894,10 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           anyfull |= full[l];
           anyface |= face[l];
         }
-        auto key_of = [](int mval, uint32_t lin) -> unsigned long long {
-          return (static_cast<unsigned long long>(static_cast<uint32_t>(mval) ^ 0x80000000u) << 32) |
-                 static_cast<unsigned long long>(0xFFFFFFFFu - lin);
-        };
-        auto lin_of = [&](int l, int P, int Q) -> uint32_t {
+        auto key_of = [](int mval, unsigned long long lin) -> unsigned long long { return best_key(mval, lin); };
+        auto lin_of = [&](int l, int P, int Q) -> unsigned long long {
           const uint32_t j = LS(l, kOrgJ) + j0 + P - 1, k = LS(l, kOrgK) + k0 + Q - 1;
-          return (static_cast<uint32_t>(si[l]) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
+          return (static_cast<unsigned long long>(static_cast<uint32_t>(si[l])) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
                      static_cast<uint32_t>(LS(l, kLenC) + 1) + k;
         };
         // Only a tile that can beat the item's best so far (its max value with

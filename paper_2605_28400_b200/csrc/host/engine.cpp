@@ -196,6 +196,7 @@ std::vector<RowsOutcome> oracle_align_batch(const std::vector<Triplet>& ts, cons
     RowsOutcome& o = outc[t];
     if (out.status[t] != TA_OK) {
       o.ok = false;
+      o.status = out.status[t];
       o.error = detail::error_message(out.status[t], ts[t], cfg, true, cell_budget);
       continue;
     }
@@ -219,7 +220,10 @@ AlignmentResult oracle_align(const Triplet& t, const ScoringScheme& scheme, Alig
                         std::to_string(cell_budget) + " (triplet '" + t.id + "')");
   }
   std::vector<RowsOutcome> o = oracle_align_batch({t}, scheme, mode, cell_budget, 0);
-  if (!o[0].ok) throw std::logic_error(o[0].error);
+  // the reference class of the failure (ParseError for a non-ACGT residue:
+  // the GPU engine packs 2-bit codes, so it is stricter than the reference's
+  // fill_tensor, which scores any character - INTEGRATION.md)
+  if (!o[0].ok) throw_status(o[0].status, o[0].error);
   AlignmentResult r = o[0].result;
   if (!with_rows) {
     r.has_rows = false;

@@ -22,6 +22,7 @@ struct RowsOutcome {
   bool ok = false;
   AlignmentResult result;
   std::string error;
+  int status = 0;  // ta_status of a failure (maps onto the reference exception class)
 };
 std::vector<RowsOutcome> oracle_align_batch(const std::vector<Triplet>& ts, const ScoringScheme& scheme,
                                             AlignmentMode mode, uint64_t cell_budget = kOracleCellBudget,

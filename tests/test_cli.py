@@ -87,3 +87,74 @@ def test_cli_capacity_errors_identical(tmp_path):
     assert r["ref"][1] == r["ours"][1]
     r = both(["oracle", "--in", "big.fa", "--cell-budget", "100", "--out", "o.csv"], tmp_path, ["o.csv"])
     assert r["ref"][1] == r["ours"][1]
+
+
+def test_accuracy_identical(tmp_path):
+    """`accuracy` (SPFP/SPFN, cli.cpp:227-258, metrics.cpp:16-60) byte for byte:
+    estimated = the reference oracle's rows, reference = the generator's true
+    alignment; plus the per-alignment 'not the same sequences' row and the
+    file-level errors (count mismatch, unequal rows, bad character)."""
+    need_ref()
+    assert run(REF, ["generate", "--spec", "uniform:0:40:120", "--rates", "0.1:0.05", "--seed", "5", "--out",
+                     "d.fa", "--ref-out", "t.fa"], tmp_path).returncode == 0
+    assert run(REF, ["oracle", "--in", "d.fa", "--mode", "local", "--rows-out", "e.fa", "--out", "o.csv"],
+               tmp_path).returncode == 0
+    # a copy of the estimate whose first alignment is over other sequences
+    lines = (tmp_path / "e.fa").read_text().splitlines()
+    for x, ln in enumerate(lines):
+        if not ln.startswith(">") and "A" in ln:
+            lines[x] = ln.replace("A", "C", 1)
+            break
+    (tmp_path / "e2.fa").write_text("\n".join(lines) + "\n")
+    (tmp_path / "short.fa").write_text(">a\nAC-\n>b\nA-C\n>c\n--AC\n")
+    (tmp_path / "bad.fa").write_text(">a\nAC-\n>b\nANC\n>c\n-AC\n")
+    (tmp_path / "two.fa").write_text(">a\nAC\n>b\nAC\n>c\nAC\n" * 2)
+    for est, ref in (("e.fa", "t.fa"), ("t.fa", "e.fa"), ("e2.fa", "t.fa"), ("t.fa", "t.fa"),
+                     ("two.fa", "t.fa"), ("short.fa", "short.fa"), ("bad.fa", "bad.fa"), ("missing.fa", "t.fa")):
+        r = both(["accuracy", "--estimated", est, "--reference", ref, "--out", "acc.csv"], tmp_path, ["acc.csv"])
+        assert r["ref"][0] == r["ours"][0], (est, ref, r["ref"][2], r["ours"][2])
+        assert r["ref"][1] == r["ours"][1], (est, ref)
+        assert r["ref"][2] == r["ours"][2], (est, ref)
+
+
+def test_fasta_parse_errors_identical_on_large_inputs(tmp_path):
+    """The parallel FASTA reader (chunks cut at headers) reports the same
+    first error, with the same line number, as the reference's getline
+    reader (fasta.cpp:11-68), including through a pipe (`--in -`)."""
+    need_ref()
+    assert run(REF, ["generate", "--spec", "fixed:150:150:150:60000", "--rates", "0.02:0.01", "--seed", "9",
+                     "--out", "d.fa"], tmp_path).returncode == 0
+    text = (tmp_path / "d.fa").read_text()
+    lines = text.splitlines()
+    # a bad residue late in the file and another one later still: the first wins
+    for at in (len(lines) * 2 // 3, len(lines) - 5):
+        while lines[at].startswith(">"):
+            at += 1
+        lines[at] = lines[at][:3] + "n" + "X" + lines[at][5:]
+    (tmp_path / "bad.fa").write_text("\r\n".join(lines) + "\r\n\n\n")
+    (tmp_path / "late_header.fa").write_text(text + ">\nACGT\n")
+    (tmp_path / "odd.fa").write_text(text + ">extra\nACGT\n")
+    for f in ("bad.fa", "late_header.fa", "odd.fa"):
+        r = both(["align", "--in", f, "--out", "a.csv"], tmp_path, [])
+        assert r["ref"][0] == r["ours"][0] == 2, (f, r["ref"][2], r["ours"][2])
+        assert r["ref"][2] == r["ours"][2], f
+    need_ref()
+    for exe in (REF, OURS):
+        p = subprocess.run(f"cat bad.fa | {exe} align --in - --out a.csv", shell=True, cwd=tmp_path,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 2 and "invalid character 'N'" in p.stderr, (exe, p.stderr)
+
+
+@pytest.mark.gpu
+def test_stdin_pipe_identical(tmp_path):
+    """`--in -` from a pipe (not seekable) reaches the engine."""
+    need_ref()
+    assert run(OURS, ["generate", "--spec", "uniform:0:80:64", "--rates", "0.1:0.02", "--seed", "4", "--out",
+                      "d.fa"], tmp_path).returncode == 0
+    outs = {}
+    for exe in (REF, OURS):
+        p = subprocess.run(f"cat d.fa | {exe} align --in - --mode semiglobal", shell=True, cwd=tmp_path,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, p.stderr
+        outs[exe] = p.stdout
+    assert outs[REF] == outs[OURS] and outs[OURS].count("\n") == 65
