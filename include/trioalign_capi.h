@@ -90,6 +90,9 @@ typedef struct {
   int64_t padded_cells;    /* cells actually swept incl. tile padding */
   int32_t lanes;           /* 1 = int32 lanes, 2 = packed s16x2 lanes */
   int32_t buckets;         /* tile-grid length buckets used */
+  int32_t reserved;
+  double walker_ms;        /* rows path: of kernel_ms, the traceback walkers */
+  int64_t dir_bytes;       /* rows path: direction-record bytes written by the wavefront */
 } ta_stats;
 
 /* ---- library / device ---------------------------------------------------- */
@@ -119,6 +122,8 @@ int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_
 int ta_batch_run(ta_batch* b, const ta_scheme* scheme, const ta_options* opt, void* stream);
 int ta_batch_fetch(ta_batch* b, ta_results* out, void* stream);
 int ta_batch_stats(const ta_batch* b, ta_stats* out);
+/* statistics of the last ta_align_batch call on a device (its internal batch) */
+int ta_last_stats(int device, ta_stats* out);
 void ta_batch_destroy(ta_batch* b);
 
 /* ---- host-side helpers with reference semantics (no GPU needed) ---------- */

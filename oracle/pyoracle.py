@@ -177,6 +177,19 @@ class Reference:
             raise RuntimeError(self.L.ref_last_error().decode())
         return score, end, status, wall.value
 
+    def oracle_align(self, t, scheme, mode: int, with_rows: bool = True, budget: int = 1 << 34):
+        """The reference oracle_align (oracle.cpp:182-190): score, end, begin, rows."""
+        res = (ctypes.c_int32 * 8)()
+        cap = len(t[0]) + len(t[1]) + len(t[2]) + 1
+        r = [ctypes.create_string_buffer(cap) for _ in range(3)]
+        rc = self.L.ref_oracle_align(t[0].encode(), len(t[0]), t[1].encode(), len(t[1]), t[2].encode(), len(t[2]),
+                                     scheme[0], scheme[1], scheme[2], mode, int(with_rows), budget, res,
+                                     r[0], r[1], r[2])
+        if rc:
+            raise RuntimeError(self.L.ref_last_error().decode())
+        return {"score": res[0], "end": list(res[1:4]), "begin": list(res[4:7]),
+                "rows": [r[d].raw[:res[7]].decode() for d in range(3)]}
+
     def generate(self, spec: str, mutation: float, indel: float, seed: int):
         s, o = ctypes.c_void_p(), ctypes.c_void_p()
         n = self.L.ref_generate(spec.encode(), mutation, indel, seed, ctypes.byref(s), ctypes.byref(o))

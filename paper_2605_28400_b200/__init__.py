@@ -24,7 +24,7 @@ __all__ = [
     "strategy_from_name", "PartitionPlan", "TripletOutcome", "WorkerStats", "BatchReport",
     "align", "align_packed", "oracle_align", "run_batch", "plan_partition", "packed_score_bound",
     "packed_bound_ok", "derive_team_width", "tcups", "align_arrays", "DeviceBatch", "lib",
-    "generate", "triplets_from_arrays", "device_count",
+    "generate", "triplets_from_arrays", "device_count", "last_stats",
     "TrioalignError", "ParseError", "CapacityError", "ConfigError", "ShapeMismatchError",
     "LaneOverflowError", "MalformedAlignmentError", "LogicError", "CudaError", "KGAP",
     "K_ORACLE_CELL_BUDGET", "LIB_PATH",
@@ -116,14 +116,15 @@ class _Stats(ctypes.Structure):
     _fields_ = [("kernel_ms", ctypes.c_double), ("wavefront_ms", ctypes.c_double),
                 ("cells", ctypes.c_int64), ("launches", ctypes.c_int64),
                 ("padded_cells", ctypes.c_int64), ("lanes", ctypes.c_int32),
-                ("buckets", ctypes.c_int32)]
+                ("buckets", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("walker_ms", ctypes.c_double), ("dir_bytes", ctypes.c_int64)]
 
 
 _LIB = None
 
 EXPORTED_SYMBOLS = (
     "ta_last_error", "ta_version", "ta_device_count", "ta_align_batch", "ta_batch_create",
-    "ta_batch_run", "ta_batch_fetch", "ta_batch_stats", "ta_batch_destroy",
+    "ta_batch_run", "ta_batch_fetch", "ta_batch_stats", "ta_last_stats", "ta_batch_destroy",
     "ta_packed_score_bound", "ta_derive_team_width", "ta_validate_scheme",
     "ta_validate_options", "ta_plan_partition", "ta_generate", "ta_generate_slice", "ta_generate_reference",
     "ta_generate_error", "ta_free",
@@ -150,6 +151,7 @@ def lib() -> ctypes.CDLL:
     L.ta_batch_run.argtypes = [vp, ctypes.POINTER(_Scheme), ctypes.POINTER(_Options), vp]
     L.ta_batch_fetch.argtypes = [vp, ctypes.POINTER(_Results), vp]
     L.ta_batch_stats.argtypes = [vp, ctypes.POINTER(_Stats)]
+    L.ta_last_stats.argtypes = [ctypes.c_int, ctypes.POINTER(_Stats)]
     L.ta_batch_destroy.argtypes = [vp]
     L.ta_batch_destroy.restype = None
     L.ta_packed_score_bound.argtypes = [i64, i64, i64, ctypes.POINTER(_Scheme)]
@@ -176,6 +178,13 @@ def lib() -> ctypes.CDLL:
 def _check(rc: int):
     if rc != 0:
         _raise(rc, lib().ta_last_error().decode(errors="replace"))
+
+
+def last_stats(device: int = 0) -> dict:
+    """Engine statistics of the last one-shot call (ta_align_batch) on a device."""
+    st = _Stats()
+    _check(lib().ta_last_stats(device, ctypes.byref(st)))
+    return {k: getattr(st, k) for k, _ in _Stats._fields_}
 
 
 def device_count() -> int:
@@ -391,10 +400,11 @@ def _options(mode, with_rows, cfg: Optional[EngineConfig], cell_budget=None) -> 
 def align_arrays(seqs: np.ndarray, offsets: np.ndarray, scheme: ScoringScheme,
                  mode: AlignmentMode = AlignmentMode.Global, cfg: Optional[EngineConfig] = None,
                  with_rows: bool = False, cell_budget: Optional[int] = None, device: int = 0,
-                 stream: Optional[int] = None) -> dict:
+                 stream: Optional[int] = None, raw_rows: bool = False) -> dict:
     """One batch through ta_align_batch.  seqs: uint8 ASCII, offsets: int64 [3n+1].
     Returns numpy arrays: score, end (n,3), status, and with rows: begin,
-    row_len, rows (list of 3-tuples of str)."""
+    row_len, rows (list of 3-tuples of str) - or, with raw_rows, the three
+    uint8 row planes and row_off (triplet t's rows start at row_off[t])."""
     L = lib()
     seqs = np.ascontiguousarray(seqs, dtype=np.uint8)
     offsets = np.ascontiguousarray(offsets, dtype=np.int64)
@@ -423,7 +433,9 @@ def align_arrays(seqs: np.ndarray, offsets: np.ndarray, scheme: ScoringScheme,
     opt = _options(mode, with_rows, cfg, cell_budget)
     _check(L.ta_align_batch(device, _ptr(seqs), _ptr(offsets), n, ctypes.byref(sch),
                             ctypes.byref(opt), ctypes.byref(res), stream))
-    if with_rows:
+    if with_rows and raw_rows:
+        out.update(begin=begin, row_len=row_len, row_off=row_off, row_planes=(r0, r1, r2))
+    elif with_rows:
         rows = []
         for t in range(n):
             o, ln = int(row_off[t]), int(row_len[t])

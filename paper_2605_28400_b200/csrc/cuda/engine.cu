@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstdio>
@@ -379,6 +380,7 @@ struct DeviceCtx {
   DevBuf<unsigned long long> d_key;
   std::vector<std::unique_ptr<BucketLaunch>> plan_pool;  // pipelined path launch plans (grow-only)
   ta_batch* oneshot = nullptr;  // reused batch object of the one-shot rows / affine path (never freed)
+  ta_stats last_stats{};        // of the last ta_align_batch call (ta_last_stats)
 };
 
 std::mutex g_ctx_mu;
@@ -511,7 +513,7 @@ struct ta_batch {
   DevBuf<uint4> d_dirs;
   DevBuf<int64_t> d_diroff, d_rowoff;
   DevBuf<char> d_rows;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evw0 = nullptr, evw1 = nullptr;
   ta_stats stats{};
   // score-path launch plans of the last run (reused while the bucket
   // contents, lanes and mode are unchanged)
@@ -529,6 +531,8 @@ struct ta_batch {
   ~ta_batch() {
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (evw0) cudaEventDestroy(evw0);
+    if (evw1) cudaEventDestroy(evw1);
   }
 };
 
@@ -1385,12 +1389,22 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     TA_CK(cudaEventSynchronize(bt->ev1));
     TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
   } else {
-    // Direction-cube chunks: (a+1) * G^2 tile-slices of 64 B per triplet.
+    // Direction-cube chunks: (a+1) * G^2 tile-slices of 64 B per triplet,
+    // sized to half the free HBM.  All chunk plans are made up front (one
+    // upload of record offsets and ids); chunks run back to back on the
+    // stream, so planning chunk k+1 on the host overlaps chunk k on the GPU.
     size_t free_b = 0, total_b = 0;
     TA_CK(cudaMemGetInfo(&free_b, &total_b));
     const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b + bt->d_dirs.cap * 16) * 0.5));
-    size_t pool_used = 0;
-    TA_CK(cudaEventRecord(bt->ev0, st));
+    struct Chunk {
+      int g;
+      size_t lo, hi;
+    };
+    std::vector<Chunk> chunks;
+    std::vector<int32_t> order;
+    order.reserve(all_ok.size());
+    std::vector<int64_t> diroff(static_cast<size_t>(n), 0);
+    size_t max_used = 0;
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       const std::vector<int32_t>& ids = buckets[size_t(gi)];
       if (ids.empty()) continue;
@@ -1398,56 +1412,72 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       const int g = ta::kGridSizes[gi];
       size_t pos = 0;
       while (pos < ids.size()) {
-        std::vector<int32_t> chunk;
-        std::vector<int64_t> diroff(static_cast<size_t>(n), 0);
+        const size_t lo = order.size();
         size_t used = 0;  // uint4 units
         while (pos < ids.size()) {
           const int32_t id = ids[pos];
           const Blocks blk = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], g);
           const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * 4;
-          if (!chunk.empty() && (used + need) * 16 > budget) break;
+          if (order.size() > lo && (used + need) * 16 > budget) break;
           diroff[size_t(id)] = int64_t(used);
           used += need;
-          chunk.push_back(id);
+          order.push_back(id);
           ++pos;
         }
-        TA_CK(bt->d_dirs.reserve(used));
-        TA_CK(bt->d_diroff.reserve(size_t(n)));
-        TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-        ta::WaveArgs args = base;
-        args.dirs = bt->d_dirs.ptr;
-        args.dir_off = bt->d_diroff.ptr;
-        if (int rc = launch_bucket(bt, chunk, g, 1, opt.mode, true, args, st, &launches, &pool_used)) return rc;
-        if (opt.mode != TA_GLOBAL) {
-          TA_CK(bt->d_ids.reserve(chunk.size()));
-          TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
-          const int64_t m = int64_t(chunk.size());
-          decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr,
-                                                                      m, bt->d_score.ptr, bt->d_end.ptr);
-          TA_CK(cudaGetLastError());
-          ++launches;
-        }
-        TA_CK(bt->d_ids.reserve(chunk.size()));
-        TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, chunk.data(), chunk.size() * 4, cudaMemcpyHostToDevice, st));
-        const int m = int(chunk.size());
-        walker_kernel<<<unsigned((m + 127) / 128), 128, 0, st>>>(
-            bt->d_desc.ptr, bt->seq.ptr, bt->d_ids.ptr, m, reinterpret_cast<const uint32_t*>(bt->d_dirs.ptr),
-            bt->d_diroff.ptr, g, opt.mode, bt->d_end.ptr, bt->d_begin.ptr, bt->d_rows.ptr, bt->d_rowoff.ptr,
-            bt->d_rowlen.ptr, bt->d_status.ptr);
+        chunks.push_back(Chunk{g, lo, order.size()});
+        max_used = std::max(max_used, used);
+        bt->stats.dir_bytes += int64_t(used) * 16;
+      }
+    }
+    TA_CK(bt->d_dirs.reserve(max_used + 1));
+    TA_CK(bt->d_diroff.reserve(size_t(n) + 1));
+    TA_CK(bt->d_ids.reserve(order.size() + 1));
+    if (!bt->evw0) TA_CK(cudaEventCreate(&bt->evw0));
+    if (!bt->evw1) TA_CK(cudaEventCreate(&bt->evw1));
+    if (n) TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    if (!order.empty())
+      TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, st));
+    size_t pool_used = 0;
+    float walker_ms = 0.f;
+    TA_CK(cudaEventRecord(bt->ev0, st));
+    for (const Chunk& ch : chunks) {
+      const std::vector<int32_t> chunk(order.begin() + std::ptrdiff_t(ch.lo), order.begin() + std::ptrdiff_t(ch.hi));
+      const int32_t* d_chunk = bt->d_ids.ptr + ch.lo;
+      const int64_t m = int64_t(chunk.size());
+      ta::WaveArgs args = base;
+      args.dirs = bt->d_dirs.ptr;
+      args.dir_off = bt->d_diroff.ptr;
+      if (int rc = launch_bucket(bt, chunk, ch.g, 1, opt.mode, true, args, st, &launches, &pool_used)) return rc;
+      if (opt.mode != TA_GLOBAL) {
+        decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, d_chunk, m,
+                                                                    bt->d_score.ptr, bt->d_end.ptr);
         TA_CK(cudaGetLastError());
         ++launches;
-        TA_CK(cudaStreamSynchronize(st));
+      }
+      const bool timed = chunks.size() == 1;  // per-chunk event sync would serialise the host
+      if (timed) TA_CK(cudaEventRecord(bt->evw0, st));
+      walker_kernel<<<unsigned((m + 127) / 128), 128, 0, st>>>(
+          bt->d_desc.ptr, bt->seq.ptr, d_chunk, int(m), reinterpret_cast<const uint32_t*>(bt->d_dirs.ptr),
+          bt->d_diroff.ptr, ch.g, opt.mode, bt->d_end.ptr, bt->d_begin.ptr, bt->d_rows.ptr, bt->d_rowoff.ptr,
+          bt->d_rowlen.ptr, bt->d_status.ptr);
+      TA_CK(cudaGetLastError());
+      ++launches;
+      if (timed) {
+        TA_CK(cudaEventRecord(bt->evw1, st));
+        TA_CK(cudaEventSynchronize(bt->evw1));
+        TA_CK(cudaEventElapsedTime(&walker_ms, bt->evw0, bt->evw1));
       }
     }
     TA_CK(cudaEventRecord(bt->ev1, st));
     TA_CK(cudaEventSynchronize(bt->ev1));
     TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
+    bt->stats.walker_ms = walker_ms;
   }
   (void)rows_out;
   int64_t cells = 0;
   for (int32_t id : all_ok) cells += int64_t(bt->a[size_t(id)]) * bt->b[size_t(id)] * bt->c[size_t(id)];
   bt->stats.kernel_ms = ms_total;
-  bt->stats.wavefront_ms = ms_total;
+  bt->stats.wavefront_ms = ms_total - bt->stats.walker_ms;
   bt->stats.cells = cells;
   bt->stats.launches = launches;
   bt->stats.lanes = lanes_used;
@@ -1514,6 +1544,20 @@ void host_pack(const char* seqs, const int64_t* offs, int64_t lo, int64_t hi, co
   std::vector<std::thread> pool;
   for (int w = 0; w < nt; ++w) pool.emplace_back(work, lo + n * w / nt, lo + n * (w + 1) / nt);
   for (auto& th : pool) th.join();
+}
+
+// Host packing threads of one pipelined call: TA_HOST_THREADS if set (e.g.
+// cores / ranks when several processes share the host), else the cores
+// divided by the calls in flight in this process (run_batch runs one call
+// per worker thread and device), so concurrent workers do not oversubscribe.
+std::atomic<int> g_calls_in_flight{0};
+int host_threads() {
+  if (const char* e = std::getenv("TA_HOST_THREADS")) {
+    const int v = std::atoi(e);
+    if (v > 0) return v;
+  }
+  const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
+  return std::max(1, hw / std::max(1, g_calls_in_flight.load()));
 }
 
 int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offsets, int64_t n,
@@ -1594,7 +1638,7 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     }
     cut.push_back(n);
   }
-  const int threads = int(std::max(1u, std::thread::hardware_concurrency()));
+  const int threads = host_threads();
   const bool prof = std::getenv("TA_PROFILE_PIPELINE") != nullptr;
   const int g2 = 2 * scheme.gap;
   ta::WaveArgs base{};
@@ -1738,6 +1782,8 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
                  ms(tq0, tq1), ms(tq1, tq2), ms(tq2, tq3), ms(tq3, std::chrono::steady_clock::now()));
   }
   if (cfg_rc) g_err = cfg_msg;
+  ctx->last_stats = ta_stats{};
+  ctx->last_stats.launches = launches;
   return TA_OK;
 }
 
@@ -1886,6 +1932,15 @@ int ta_batch_fetch(ta_batch* b, ta_results* out, void* stream) {
   return TA_OK;
 }
 
+int ta_last_stats(int device, ta_stats* out) {
+  if (!out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
+  DeviceCtx* ctx = nullptr;
+  if (int rc = get_ctx(device, &ctx)) return rc;
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  *out = ctx->last_stats;
+  return TA_OK;
+}
+
 int ta_batch_stats(const ta_batch* b, ta_stats* out) {
   if (!b || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
   *out = b->stats;
@@ -1907,6 +1962,10 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
     DeviceCtx* ctx = nullptr;
     if (int rc = get_ctx(device, &ctx)) return rc;
     cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    struct InFlight {
+      InFlight() { ++g_calls_in_flight; }
+      ~InFlight() { --g_calls_in_flight; }
+    } in_flight;
     return align_scores_pipelined(ctx, seqs, offsets, n, *scheme, *opt, out, st);
   }
   // One cached batch object per device: its device buffers (sequences,
@@ -1920,6 +1979,7 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
   if (int rc = batch_init(bt, ctx, device, seqs, offsets, n, st)) return rc;
   if (!opt->with_rows) {
     if (int rc = run_impl(bt, *scheme, *opt, st, nullptr)) return rc;
+    ctx->last_stats = bt->stats;
     return ta_batch_fetch(bt, out, stream);
   }
   // rows path: device row buffers sized a+b+c per row
@@ -1939,6 +1999,7 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
   TA_CK(cudaMemsetAsync(bt->d_status.ptr, 0, nn * 4, st));
   if (nn) TA_CK(cudaMemcpyAsync(bt->d_rowoff.ptr, roff.data(), nn * 8, cudaMemcpyHostToDevice, st));
   if (int rc = run_impl(bt, *scheme, *opt, st, out)) return rc;
+  ctx->last_stats = bt->stats;
   if (nn == 0) return TA_OK;
   std::vector<int32_t> dstat(nn), rlen(nn), beg(3 * nn);
   std::vector<char> rows(size_t(total) + 1);

@@ -103,3 +103,33 @@ def test_weak_scaling_shards_extend_the_single_gpu_workload():
         assert len(offs) == 3 * n + 1
         if rank == 0:
             assert seqs[:int(offs[-1])].tobytes() == one[:int(one_off[-1])].tobytes()
+
+
+@pytest.mark.parametrize("scaling,total", [("strong", 1000000), ("weak", 2000000)])
+def test_bench_launcher_world2(scaling, total):
+    """`bench.py --gpus 2` without torchrun re-launches itself through
+    torch.distributed.run (2 ranks, 127.0.0.1); --dry-run runs the real
+    launcher, shard plan and max / sum reductions on gloo without a GPU."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run",
+                        "--scaling", scaling], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == scaling
+    assert line["total_triplets"] == total and line["covered"] == total and line["max_hi"] == total
+    assert line["rank0_shard"] == [0, total // 2] and line["max_rank"] == 1
+
+
+def test_bench_refuses_missing_gpus():
+    """Without enough visible GPUs, --gpus N fails instead of silently
+    reporting n_gpus 1."""
+    import json
+    import subprocess
+    import torch
+    if torch.cuda.device_count() >= 4:
+        pytest.skip("4 GPUs visible")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4", "--no-e2e"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode != 0
+    assert "GPU(s) visible" in json.loads(r.stdout.strip().splitlines()[-1])["error"]
