@@ -169,16 +169,19 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
   const ta::TripletDesc d = desc[id];
   constexpr int N = ta::kTileN;
   const int T = grid * grid;
-  const uint32_t* base = dirs + dir_off[id] * 4;
+  const uint32_t* base = dirs + dir_off[id];
   const int GN = grid * N;
   const int Bk = (d.c + 1 + GN - 1) / GN;
+  // record layout (wavefront.cuh, kDirWords): [block][slice][word][thread],
+  // thread = anti-diagonal index of the tile, word/bit = sweep-order index of the cell
   auto code_at = [&](int i, int j, int k) -> uint32_t {
     const int blk = (j / GN) * Bk + (k / GN);
     const int jj = j % GN, kk = k % GN;
-    const int t = (jj / N) * grid + (kk / N);
-    const int cell = (jj % N) * N + (kk % N);
-    const uint32_t w = base[((int64_t(blk) * (d.a + 1) + i) * T + t) * 16 + (cell >> 3)];
-    return (w >> ((cell & 7) * 4)) & 15u;
+    const int t = ta::antidiag_index(jj / N, kk / N, grid);
+    const int cs = ta::antidiag_index(jj % N, kk % N, N);
+    const int m = cs % 10;
+    const uint32_t w = base[((int64_t(blk) * (d.a + 1) + i) * ta::kDirWords + cs / 10) * T + t];
+    return (w >> (m < 5 ? 3 * m : 16 + 3 * (m - 5))) & 7u;
   };
   auto stop_at = [&](int i, int j, int k, uint32_t code) {
     if (mode == ta::kGlobal) return i == 0 && j == 0 && k == 0;
@@ -468,6 +471,15 @@ bool s16_ok(const ta_scheme& s, int64_t max_bound) {
   if (mm < 0 || mp > 127) return false;  // carry-free packed adds + byte tables
   // values in [0, bound]; unreachable terms stay below 0 from NEG = -16384
   return max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kTileN <= 32000;
+}
+
+// TRACE kernels scale values by 8 (3-bit direction tags in the low bits):
+// s16x2 lanes need the scaled bound to fit as well.
+bool trace16_ok(const ta_scheme& s, int64_t max_bound) {
+  const int g2 = 2 * s.gap;
+  const int mp = s.match - g2, mm = s.mismatch - g2;
+  if (mm < 0 || mp > 127) return false;
+  return (max_bound + 3 * 127 + int64_t(-g2) * 2 * ta::kTileN) * 8 + 64 <= 32000;
 }
 
 // Semi-global / local best-cell keys (ta::best_key) hold 36 bits of cell
@@ -1399,6 +1411,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     struct Chunk {
       int g;
       size_t lo, hi;
+      int lanes;
     };
     std::vector<Chunk> chunks;
     std::vector<int32_t> order;
@@ -1417,19 +1430,19 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
         while (pos < ids.size()) {
           const int32_t id = ids[pos];
           const Blocks blk = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], g);
-          const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * 4;
-          if (order.size() > lo && (used + need) * 16 > budget) break;
+          const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * ta::kDirWords;
+          if (order.size() > lo && (used + need) * 4 > budget) break;
           diroff[size_t(id)] = int64_t(used);
           used += need;
           order.push_back(id);
           ++pos;
         }
-        chunks.push_back(Chunk{g, lo, order.size()});
+        chunks.push_back(Chunk{g, lo, order.size(), trace16_ok(scheme, max_bound_bucket[gi]) ? 2 : 1});
         max_used = std::max(max_used, used);
-        bt->stats.dir_bytes += int64_t(used) * 16;
+        bt->stats.dir_bytes += int64_t(used) * 4;
       }
     }
-    TA_CK(bt->d_dirs.reserve(max_used + 1));
+    TA_CK(bt->d_dirs.reserve(max_used / 4 + 1));
     TA_CK(bt->d_diroff.reserve(size_t(n) + 1));
     TA_CK(bt->d_ids.reserve(order.size() + 1));
     if (!bt->evw0) TA_CK(cudaEventCreate(&bt->evw0));
@@ -1445,9 +1458,10 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       const int32_t* d_chunk = bt->d_ids.ptr + ch.lo;
       const int64_t m = int64_t(chunk.size());
       ta::WaveArgs args = base;
-      args.dirs = bt->d_dirs.ptr;
+      args.dirs = reinterpret_cast<uint32_t*>(bt->d_dirs.ptr);
       args.dir_off = bt->d_diroff.ptr;
-      if (int rc = launch_bucket(bt, chunk, ch.g, 1, opt.mode, true, args, st, &launches, &pool_used)) return rc;
+      if (int rc = launch_bucket(bt, chunk, ch.g, ch.lanes, opt.mode, true, args, st, &launches, &pool_used)) return rc;
+      lanes_used = std::max(lanes_used, ch.lanes);
       if (opt.mode != TA_GLOBAL) {
         decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, d_chunk, m,
                                                                     bt->d_score.ptr, bt->d_end.ptr);

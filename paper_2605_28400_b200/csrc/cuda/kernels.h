@@ -24,7 +24,7 @@ struct KernelEntry {
   int grid = 0;
 };
 
-// lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace requires lanes == 1;
+// lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace with either lane width;
 // blk: 0 single-plane, 1 sequential multi-block items, 2 wave (multi-CTA)
 // blocks; blk > 0 exists for the largest grid only, blk == 2 without trace.
 KernelEntry kernel_g4(int lanes, int mode, bool trace, int blk);
@@ -57,11 +57,18 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
   template <int BL>                                                                    \
   static KernelEntry pick_##G(int lanes, int mode, bool trace) {                       \
     if (trace) {                                                                       \
-      if (lanes != 1) return {};                                                       \
-      switch (mode) {                                                                  \
-        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, true, BL);                 \
-        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, true, BL);                     \
-        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, true, BL);                   \
+      if (lanes == 1) {                                                                \
+        switch (mode) {                                                                \
+          case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, true, BL);               \
+          case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, true, BL);                   \
+          case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, true, BL);                 \
+        }                                                                              \
+      } else {                                                                         \
+        switch (mode) {                                                                \
+          case kGlobal: return TA_KERNEL_ENTRY(G, 2, kGlobal, true, BL);               \
+          case kSemi: return TA_KERNEL_ENTRY(G, 2, kSemi, true, BL);                   \
+          case kLocal: return TA_KERNEL_ENTRY(G, 2, kLocal, true, BL);                 \
+        }                                                                              \
       }                                                                                \
       return {};                                                                       \
     }                                                                                  \

@@ -40,11 +40,27 @@ constexpr int kGlobal = 0;
 constexpr int kSemi = 1;
 constexpr int kLocal = 2;
 
-// Direction tags carried in the 4 low bits of TRACE values.  Larger tag wins
-// ties, so the max selects the FIRST term of Eq. 1 in listed order
-// (oracle.cpp:124-144).  15 = local-mode floor (stop, oracle.cpp:109-110).
-constexpr uint32_t kTagT1 = 12, kTagT2 = 5, kTagT3 = 4, kTagT4 = 3;
-constexpr uint32_t kTagT5 = 2, kTagT6 = 1, kTagT7 = 0, kTagStop = 15;
+// Direction tags carried in the 3 low bits of TRACE values (values scaled by
+// 8, so both int32 and s16x2 lanes trace).  Larger tag wins ties, so the max
+// selects the FIRST term of Eq. 1 in listed order (oracle.cpp:124-144).
+// 7 = local-mode floor (stop, oracle.cpp:109-110).
+constexpr uint32_t kTagT1 = 6, kTagT2 = 5, kTagT3 = 4, kTagT4 = 3;
+constexpr uint32_t kTagT5 = 2, kTagT6 = 1, kTagT7 = 0, kTagStop = 7;
+// Direction records: per (lane triplet, block, slice, tile) kDirWords 32-bit
+// words, stored [word][thread] so a warp's stores are 128 B contiguous.  Word
+// w holds the 3-bit codes of sweep-order cells 10w .. 10w+9: cell m < 5 at
+// bit 3m, cell m >= 5 at bit 16 + 3(m - 5) (two 15-bit halves).
+constexpr int kDirWords = 10;
+constexpr uint32_t kTraceC1 = 0xFFFFFFFAu;  // int32 lanes: -6
+constexpr uint32_t kTraceC2 = 0xFFF9FFFAu;  // s16x2 lanes: -6 per lane (the low lane always carries)
+// Sweep-order index of cell (p, q) of an n x n tile visited by anti-diagonals
+// (d = p + q, p ascending); with n = G it is the thread index of tile (r, c)
+// under the kernel's anti-diagonal thread map.
+__host__ __device__ inline int antidiag_index(int p, int q, int n) {
+  const int d = p + q;
+  const int before = d <= n - 1 ? d * (d + 1) / 2 : n * (n + 1) / 2 + (n * (n - 1) - (2 * n - d) * (2 * n - d - 1)) / 2;
+  return before + p - (d > n - 1 ? d - (n - 1) : 0);
+}
 
 // Semi-global / local best-cell key (optimal_score, oracle.cpp:67-88): one
 // 64-bit word that orders by larger value, then smaller lexicographic (i, j, k)
@@ -80,8 +96,8 @@ struct WaveArgs {
   int32_t* __restrict__ out_score;
   int32_t* __restrict__ out_end;           // 3 per triplet
   unsigned long long* __restrict__ out_key;  // semi/local (value, lex index)
-  uint4* __restrict__ dirs;                // TRACE: direction cube
-  const int64_t* __restrict__ dir_off;     // TRACE: per triplet, in uint4
+  uint32_t* __restrict__ dirs;             // TRACE: direction records (kDirWords per tile-slice)
+  const int64_t* __restrict__ dir_off;     // TRACE: per triplet, in 32-bit words
   int32_t match_p;                         // sigma' of equal residues   (match - g2)
   int32_t mismatch_p;                      // sigma' of unequal residues (mismatch - g2)
   int32_t g2;                              // 2 * gap (<= 0)
@@ -259,17 +275,16 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   constexpr bool BLOCKS = BLK != 0;
   constexpr bool WAVE = BLK == 2;
   static_assert(N + 1 <= kSegE, "face segment too small");
-  static_assert(!TRACE || LANES == 1, "direction cube uses int32 lanes");
   static_assert((N * N) % 4 == 0, "tile cells must group by 4");
-  static_assert(N <= 15, "a tile row's codes must fit one 32-bit word");
-  static_assert(!TRACE || (N * N) <= 128, "direction slot is 64 B per tile-slice");
+  static_assert(!TRACE || N * N == 10 * kDirWords, "direction records hold 10 cells per word");
   using Ops = LaneOps<LANES>;
   using SM = WaveSmem<N, G, LANES>;
   constexpr int T = SM::T;
-  constexpr int NN = SM::NN;
+  [[maybe_unused]] constexpr int NN = SM::NN;
   constexpr int XW = SM::XW;
-  constexpr int SH = TRACE ? 4 : 0;  // value scale 2^SH (tags in low bits)
-  constexpr uint32_t NEG = TRACE ? 0xF0000000u : Ops::kNeg;
+  constexpr int SH = TRACE ? 3 : 0;  // value scale 2^SH (tags in low bits)
+  constexpr uint32_t NEG = (TRACE && LANES == 1) ? 0xF0000000u : Ops::kNeg;
+  constexpr uint32_t kOneL = Ops::kOne;  // 1 per lane
   constexpr uint32_t kDone = 1u, kOwner = 2u;
   constexpr uint32_t kInTop = 8u, kInLeft = 16u, kOutDown = 32u, kOutRight = 64u;
 
@@ -314,6 +329,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   const int g2 = args.g2;
   const int ag2 = -g2;
   const uint32_t one = args.one;
+  // TRACE: run-time powers of two and -1 keep the record packing on the FMA pipe
+  [[maybe_unused]] const uint32_t mone = 0u - one;
+  [[maybe_unused]] const uint32_t pw[5] = {one, one << 3, one << 6, one << 9, one << 12};
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
   for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
@@ -421,7 +439,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         reinterpret_cast<uint2*>(tab1)[p * T + t] = make_uint2(v1[0] | (v1[1] << 16), v1[2] | (v1[3] << 16));
         reinterpret_cast<uint2*>(tab2)[p * T + t] = make_uint2(v2[0] | (v2[1] << 16), v2[2] | (v2[3] << 16));
       }
-      const int sc = TRACE ? 16 : 1;
+      const int sc = TRACE ? 8 : 1;
       const int tg = TRACE ? static_cast<int>(kTagT4) : 0;
       // sigma12' in the sweep's anti-diagonal cell order, 4 cells per STS.128
       uint32_t v[4];
@@ -459,8 +477,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           if (q < 0 || q >= N) continue;
           const uint32_t x1 = (c1 >> (2 * p)) & 3u;
           const uint32_t sel = x1 | ((x1 | 8u) << 4);
-          s12h[((size_t(k >> 2) * T + t) * 4 + (k & 3)) * 2 + l] =
-              ((ld.v1 >> p) & 1u) ? static_cast<uint16_t>(prmt(t2w[q], 0u, sel)) : uint16_t(0);
+          const uint32_t sv = ((ld.v1 >> p) & 1u) ? (prmt(t2w[q], 0u, sel) & 0xFFFFu) : 0u;
+          s12h[((size_t(k >> 2) * T + t) * 4 + (k & 3)) * 2 + l] = static_cast<uint16_t>(TRACE ? sv * 8u + kTagT4 : sv);
           ++k;
         }
     }
@@ -498,6 +516,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         const int q = d - p;
         if (q < 0 || q >= N) continue;
         v[k & 3] = prmt(t2a[q], t2b[q], sel[p]) & pm[p];
+        if constexpr (TRACE) v[k & 3] = v[k & 3] * 8u + kTagT4 * kOneL;
         if ((k & 3) == 3) s12v[(k >> 2) * T + t] = make_uint4(v[0], v[1], v[2], v[3]);
         ++k;
       }
@@ -563,9 +582,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     }
     if (active) {
      if (work) {
-      constexpr int NW = (NN + 7) / 8;
       uint32_t Cu[N + 1][N + 1];
-      uint32_t dirw[TRACE ? NW : 1];
       // ---- 1. new halos (published by the neighbours at step s-1) --------
       const uint32_t* xin = xbuf + (buf ^ 1) * XW * (T + 1);
 #pragma unroll
@@ -654,8 +671,18 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
       for (int q = 0; q < N; ++q) {
         s02[q] = sig_row(tab2, q);
-        if constexpr (TRACE) s02[q] = s02[q] * 16u + kTagT3;
+        if constexpr (TRACE) s02[q] = s02[q] * 8u + kTagT3 * kOneL;
       }
+      // t1's column term: sigma02' with tag 4 - 6, so that t1 = Pv + a1 + a2c + sg
+      // carries tag 5 + 4 - 6 + 3 = 6 (added on the FMA pipe: the -6 per lane
+      // is exact because every low-lane sum it meets is >= 9 or NEG-derived)
+      [[maybe_unused]] uint32_t a2c[TRACE ? N : 1];
+#ifndef TA_TRACE_Y3
+      if constexpr (TRACE) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) a2c[q] = s02[q] + (LANES == 2 ? kTraceC2 : kTraceC1);
+      }
+#endif
 
       // ---- 3. forced cells (reference initialisation, oracle.cpp:30-39) --
       // global: M(0,0,0) = 0; semi: axis cells are 0 in M-space.
@@ -702,14 +729,26 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       }
 
       // ---- 4. the tile: 6 integer instructions per cell -----------------
+      // TRACE: direction records of this step, one pointer per live lane
+      [[maybe_unused]] uint32_t* dptr[LANES];
+      [[maybe_unused]] bool dok[LANES];
       if constexpr (TRACE) {
 #pragma unroll
-        for (int w = 0; w < NW; ++w) dirw[w] = 0;
+        for (int l = 0; l < LANES; ++l) {
+          dok[l] = !(flags[l] & kDone) && si[l] <= la[l] && LS(l, kTid) >= 0;
+          dptr[l] = args.dirs;
+          if (dok[l]) {
+            const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+            dptr[l] = args.dirs + args.dir_off[LS(l, kTid)] +
+                      (static_cast<int64_t>(blk) * (la[l] + 1) + si[l]) * (kDirWords * T) + t;
+          }
+        }
       }
+      [[maybe_unused]] uint32_t accA = 0, accB = 0;
       // local floor |g2| * (i + j + k) of the current cell, stepped along the
       // row on the FMA pipe (values >= 0: packed adds never carry)
       const uint32_t ag2s = Ops::splat(ag2 * (1 << SH));
-      uint32_t flrow = flbase + (TRACE ? kTagStop : 0u);
+      uint32_t flrow = flbase + (TRACE ? kTagStop * kOneL : 0u);
       auto sweep_tile = [&]() {
       // Cells in anti-diagonal order (d = P + Q): consecutive cells are
       // independent, so the row / column dependencies of the recurrence are
@@ -719,7 +758,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
       for (int p = 0; p < N; ++p) {
         a1v[p] = sig_row(tab1, p);
-        if constexpr (TRACE) a1v[p] = a1v[p] * 16u + kTagT2;
+        if constexpr (TRACE) a1v[p] = a1v[p] * 8u + kTagT2 * kOneL;
       }
       uint4 sg4 = make_uint4(0, 0, 0, 0);
       [[maybe_unused]] uint32_t fd = flrow;  // local floor of diagonal d (depends on P + Q only)
@@ -735,9 +774,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const int Q0 = d - P0;
           if (Q0 < 0 || Q0 >= N) continue;
           const int P = P0 + 1, Q = Q0 + 1;
-          const int cell = (P - 1) * N + (Q - 1);
           if ((k & 3) == 0) sg4 = s12v[(k >> 2) * T + t];
           const uint32_t sg = (k & 3) == 0 ? sg4.x : (k & 3) == 1 ? sg4.y : (k & 3) == 2 ? sg4.z : sg4.w;
+          [[maybe_unused]] const int ks = k;  // sweep-order index of this cell
           ++k;
           const uint32_t a1 = a1v[P - 1];
           const uint32_t a2 = s02[Q - 1];
@@ -750,14 +789,19 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             x = Ops::addmax(Cu[P - 1][Q - 1], sg, x);                // t4
             x = Ops::max3(x, Cu[P - 1][Q], Cu[P][Q - 1]);            // t6, t7
           } else {
-            // tags: t1 = 5+4+3 = 12 (a1, a2, sg carry 5, 4, 3)
-            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2);
+            // tags: a1, a2, sg carry 5, 4, 3; t1 = 5 + (4 - 6) + 3 = 6
+#ifdef TA_TRACE_Y3
+            const uint32_t y = fma_add(fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2), one,
+                                       LANES == 2 ? kTraceC2 : kTraceC1);
+#else
+            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2c[Q - 1]);
+#endif
             x = Ops::addmax(Pv[P - 1][Q], a1, Cu[P][Q - 1]);         // max(t2, t7)
             x = Ops::addmax(Pv[P][Q - 1], a2, x);                    // t3
             x = Ops::addmax(y, sg, x);                               // t1
             x = Ops::addmax(Cu[P - 1][Q - 1], sg, x);                // t4
-            x = Ops::addmax(Pv[P][Q], kTagT5, x);                    // t5
-            x = Ops::addmax(Cu[P - 1][Q], kTagT6, x);                // t6
+            x = Ops::addmax(Pv[P][Q], kTagT5 * kOneL, x);            // t5
+            x = Ops::addmax(Cu[P - 1][Q], kTagT6 * kOneL, x);        // t6
           }
           if constexpr (MODE == kLocal) x = Ops::addmax(fd, one ^ 1u, x);  // floor 0 (oracle.cpp:59), fused form
           if constexpr (MODE == kGlobal || MODE == kSemi) {
@@ -775,8 +819,21 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             }
           }
           if constexpr (TRACE) {
-            dirw[cell >> 3] |= (x & 15u) << ((cell & 7) * 4);
-            x &= ~15u;
+            // tag -> record (IMAD accumulation on the FMA pipe), value := x - tag
+            const uint32_t code = x & (7u * kOneL);
+            x = fma_add(code, mone, x);
+            const int m = ks % 10;
+            if (m == 0) accA = code;
+            else if (m < 5) accA = fma_add(code, pw[m], accA);
+            else if (m == 5) accB = code;
+            else accB = fma_add(code, pw[m - 5], accB);
+            if (m == 9) {
+              const int w = ks / 10;
+              if (dok[0]) dptr[0][w * T] = prmt(accA, accB, 0x5410u);
+              if constexpr (LANES == 2) {
+                if (dok[LANES - 1]) dptr[LANES - 1][w * T] = prmt(accA, accB, 0x7632u);
+              }
+            }
           }
           Cu[P][Q] = x;
         }
@@ -831,23 +888,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         if (wrote) __threadfence_block();
       }
       mbar_arrive_group(&mbar[buf]);
-
-      // ---- 6. direction cube slot (64 B per tile-slice) -----------------
-      if constexpr (TRACE) {
-        if (!(flags[0] & kDone) && si[0] <= la[0] && LS(0, kTid) >= 0) {
-          const int a1 = la[0] + 1;
-          const int blk = (LS(0, kOrgJ) / GN) * LS(0, kBk) + LS(0, kOrgK) / GN;
-          uint4* dst = args.dirs + args.dir_off[LS(0, kTid)] + ((size_t(blk) * a1 + si[0]) * T + tile) * 4;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            if (v * 4 < NW) {
-              dst[v] = make_uint4(dirw[v * 4], v * 4 + 1 < NW ? dirw[(v * 4 + 1) % NW] : 0u,
-                                  v * 4 + 2 < NW ? dirw[(v * 4 + 2) % NW] : 0u,
-                                  v * 4 + 3 < NW ? dirw[(v * 4 + 3) % NW] : 0u);
-            }
-          }
-        }
-      }
 
       // ---- 7. score extraction ------------------------------------------
       if constexpr (MODE == kGlobal) {
