@@ -162,7 +162,8 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
                               const int64_t* __restrict__ dir_off, int grid, int mode,
                               const int32_t* __restrict__ end, int32_t* __restrict__ begin,
                               char* __restrict__ rows, const int64_t* __restrict__ row_off,
-                              int32_t* __restrict__ row_len, int32_t* __restrict__ status) {
+                              int32_t* __restrict__ row_len, int32_t* __restrict__ status,
+                              int32_t* __restrict__ len_ord) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
   const int id = ids[x];
@@ -217,6 +218,7 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
   if (!ok) {
     status[id] = TA_ERR_LOGIC;
     row_len[id] = 0;
+    if (len_ord) len_ord[x] = 0;
     return;
   }
   begin[3 * id] = i, begin[3 * id + 1] = j, begin[3 * id + 2] = k;
@@ -226,6 +228,7 @@ __global__ void walker_kernel(const ta::TripletDesc* __restrict__ desc,
   const int suffix = semi ? ((d.a - ei) + (d.b - ej) + (d.c - ek)) : 0;
   const int len = prefix + steps + suffix;
   row_len[id] = len;
+  if (len_ord) len_ord[x] = len;
   const int64_t cap = int64_t(d.a) + d.b + d.c;
   char* r0 = rows + row_off[id];
   char* r1 = r0 + cap;
@@ -384,6 +387,8 @@ struct DeviceCtx {
   std::vector<std::unique_ptr<BucketLaunch>> plan_pool;  // pipelined path launch plans (grow-only)
   ta_batch* oneshot = nullptr;  // reused batch object of the one-shot rows / affine path (never freed)
   ta_stats last_stats{};        // of the last ta_align_batch call (ta_last_stats)
+  PinnedBuf<char> h_rows[2];    // rows path: double-buffered D2H staging of row chunks
+  PinnedBuf<int32_t> h_len[2];
 };
 
 std::mutex g_ctx_mu;
@@ -413,6 +418,20 @@ int get_ctx(int device, DeviceCtx** out) {
   TA_CK(cudaSetDevice(device));
   *out = g_ctx[device].get();
   return TA_OK;
+}
+
+// Host packing threads of one pipelined call: TA_HOST_THREADS if set (e.g.
+// cores / ranks when several processes share the host), else the cores
+// divided by the calls in flight in this process (run_batch runs one call
+// per worker thread and device), so concurrent workers do not oversubscribe.
+std::atomic<int> g_calls_in_flight{0};
+int host_threads() {
+  if (const char* e = std::getenv("TA_HOST_THREADS")) {
+    const int v = std::atoi(e);
+    if (v > 0) return v;
+  }
+  const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
+  return std::max(1, hw / std::max(1, g_calls_in_flight.load()));
 }
 
 // ---------------------------------------------------------------------------
@@ -525,7 +544,10 @@ struct ta_batch {
   DevBuf<uint4> d_dirs;
   DevBuf<int64_t> d_diroff, d_rowoff;
   DevBuf<char> d_rows;
+  DevBuf<int32_t> d_lenord;            // rows path: row length per position of the chunk order
+  bool rows_scattered = false;         // rows path: the pipeline already wrote the caller's row planes
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evw0 = nullptr, evw1 = nullptr;
+  cudaEvent_t evk[2] = {nullptr, nullptr}, evc[2] = {nullptr, nullptr};
   ta_stats stats{};
   // score-path launch plans of the last run (reused while the bucket
   // contents, lanes and mode are unchanged)
@@ -545,6 +567,10 @@ struct ta_batch {
     if (ev1) cudaEventDestroy(ev1);
     if (evw0) cudaEventDestroy(evw0);
     if (evw1) cudaEventDestroy(evw1);
+    for (auto e : evk)
+      if (e) cudaEventDestroy(e);
+    for (auto e : evc)
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -1401,23 +1427,30 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     TA_CK(cudaEventSynchronize(bt->ev1));
     TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
   } else {
-    // Direction-cube chunks: (a+1) * G^2 tile-slices of 64 B per triplet,
-    // sized to half the free HBM.  All chunk plans are made up front (one
-    // upload of record offsets and ids); chunks run back to back on the
-    // stream, so planning chunk k+1 on the host overlaps chunk k on the GPU.
+    // Direction-record chunks: (a+1) * G^2 tile-slices of 40 B per triplet,
+    // sized to half the free HBM and - when rows go back to a host caller -
+    // to at most 1/8 of the batch, so the D2H of chunk k's rows and their
+    // scatter into the caller's row planes overlap chunk k+1's kernels.  All
+    // chunk plans are made up front (one upload of record offsets, ids and
+    // row offsets); chunks run back to back on the stream.
     size_t free_b = 0, total_b = 0;
     TA_CK(cudaMemGetInfo(&free_b, &total_b));
     const size_t budget = std::max<size_t>(size_t(1) << 28, size_t(double(free_b + bt->d_dirs.cap * 16) * 0.5));
+    const bool scatter = rows_out && rows_out->rows0 && rows_out->rows1 && rows_out->rows2 && rows_out->row_offsets;
+    const size_t pipe_max = scatter ? std::max<size_t>(4096, (all_ok.size() + 7) / 8) : SIZE_MAX;
     struct Chunk {
       int g;
       size_t lo, hi;
       int lanes;
+      int64_t rlo, rhi;  // device row bytes of the chunk
     };
     std::vector<Chunk> chunks;
     std::vector<int32_t> order;
     order.reserve(all_ok.size());
-    std::vector<int64_t> diroff(static_cast<size_t>(n), 0);
+    std::vector<int64_t> diroff(static_cast<size_t>(n), 0), roff(static_cast<size_t>(n), 0);
     size_t max_used = 0;
+    int64_t rtot = 0, max_rbytes = 0;
+    size_t max_chunk = 0;
     for (int gi = 0; gi < ta::kNumGrid; ++gi) {
       const std::vector<int32_t>& ids = buckets[size_t(gi)];
       if (ids.empty()) continue;
@@ -1426,34 +1459,83 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       size_t pos = 0;
       while (pos < ids.size()) {
         const size_t lo = order.size();
-        size_t used = 0;  // uint4 units
-        while (pos < ids.size()) {
+        const int64_t rlo = rtot;
+        size_t used = 0;  // 32-bit words
+        while (pos < ids.size() && order.size() - lo < pipe_max) {
           const int32_t id = ids[pos];
           const Blocks blk = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], g);
           const size_t need = size_t(blk.bj) * blk.bk * size_t(bt->a[size_t(id)] + 1) * size_t(g) * g * ta::kDirWords;
           if (order.size() > lo && (used + need) * 4 > budget) break;
           diroff[size_t(id)] = int64_t(used);
           used += need;
+          roff[size_t(id)] = rtot;
+          rtot += 3 * (int64_t(bt->a[size_t(id)]) + bt->b[size_t(id)] + bt->c[size_t(id)]);
           order.push_back(id);
           ++pos;
         }
-        chunks.push_back(Chunk{g, lo, order.size(), trace16_ok(scheme, max_bound_bucket[gi]) ? 2 : 1});
+        chunks.push_back(Chunk{g, lo, order.size(), trace16_ok(scheme, max_bound_bucket[gi]) ? 2 : 1, rlo, rtot});
         max_used = std::max(max_used, used);
+        max_rbytes = std::max(max_rbytes, rtot - rlo);
+        max_chunk = std::max(max_chunk, order.size() - lo);
         bt->stats.dir_bytes += int64_t(used) * 4;
       }
     }
     TA_CK(bt->d_dirs.reserve(max_used / 4 + 1));
     TA_CK(bt->d_diroff.reserve(size_t(n) + 1));
     TA_CK(bt->d_ids.reserve(order.size() + 1));
+    TA_CK(bt->d_lenord.reserve(order.size() + 1));
+    TA_CK(bt->d_rows.reserve(size_t(rtot) + 1));
+    TA_CK(bt->d_rowoff.reserve(size_t(n) + 1));
     if (!bt->evw0) TA_CK(cudaEventCreate(&bt->evw0));
     if (!bt->evw1) TA_CK(cudaEventCreate(&bt->evw1));
-    if (n) TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < 2; ++k) {
+      if (!bt->evk[k]) TA_CK(cudaEventCreateWithFlags(&bt->evk[k], cudaEventDisableTiming));
+      if (!bt->evc[k]) TA_CK(cudaEventCreateWithFlags(&bt->evc[k], cudaEventDisableTiming));
+    }
+    DeviceCtx* ctx = bt->ctx;
+    if (scatter) {
+      for (int k = 0; k < 2 && chunks.size() > size_t(k); ++k) {
+        TA_CK(ctx->h_rows[k].reserve(size_t(max_rbytes) + 1));
+        TA_CK(ctx->h_len[k].reserve(max_chunk + 1));
+      }
+    }
+    if (n) {
+      TA_CK(cudaMemcpyAsync(bt->d_diroff.ptr, diroff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+      TA_CK(cudaMemcpyAsync(bt->d_rowoff.ptr, roff.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    }
     if (!order.empty())
       TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, st));
+    // host side of the pipeline: copy chunk c's rows out of its staging slot
+    auto scatter_chunk = [&](size_t c) -> int {
+      const Chunk& ch = chunks[c];
+      TA_CK(cudaEventSynchronize(bt->evc[c & 1]));
+      const char* src = ctx->h_rows[c & 1].ptr;
+      const int32_t* len = ctx->h_len[c & 1].ptr;
+      auto copy_range = [&](size_t x0, size_t x1) {
+        for (size_t x = x0; x < x1; ++x) {
+          const int32_t id = order[ch.lo + x];
+          const int64_t cap = int64_t(bt->a[size_t(id)]) + bt->b[size_t(id)] + bt->c[size_t(id)];
+          const char* r = src + (roff[size_t(id)] - ch.rlo);
+          const int64_t o = rows_out->row_offsets[id];
+          const size_t L = size_t(len[x]);
+          std::memcpy(rows_out->rows0 + o, r, L);
+          std::memcpy(rows_out->rows1 + o, r + cap, L);
+          std::memcpy(rows_out->rows2 + o, r + 2 * cap, L);
+        }
+      };
+      const size_t m = ch.hi - ch.lo;
+      const int nt = int(std::min<size_t>(size_t(std::max(1, host_threads() / 2)), m / 4096 + 1));
+      std::vector<std::thread> pool;
+      for (int w = 1; w < nt; ++w) pool.emplace_back(copy_range, m * size_t(w) / size_t(nt), m * size_t(w + 1) / size_t(nt));
+      copy_range(0, m / size_t(nt));
+      for (auto& th : pool) th.join();
+      return TA_OK;
+    };
     size_t pool_used = 0;
     float walker_ms = 0.f;
     TA_CK(cudaEventRecord(bt->ev0, st));
-    for (const Chunk& ch : chunks) {
+    for (size_t c = 0; c < chunks.size(); ++c) {
+      const Chunk& ch = chunks[c];
       const std::vector<int32_t> chunk(order.begin() + std::ptrdiff_t(ch.lo), order.begin() + std::ptrdiff_t(ch.hi));
       const int32_t* d_chunk = bt->d_ids.ptr + ch.lo;
       const int64_t m = int64_t(chunk.size());
@@ -1473,19 +1555,33 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       walker_kernel<<<unsigned((m + 127) / 128), 128, 0, st>>>(
           bt->d_desc.ptr, bt->seq.ptr, d_chunk, int(m), reinterpret_cast<const uint32_t*>(bt->d_dirs.ptr),
           bt->d_diroff.ptr, ch.g, opt.mode, bt->d_end.ptr, bt->d_begin.ptr, bt->d_rows.ptr, bt->d_rowoff.ptr,
-          bt->d_rowlen.ptr, bt->d_status.ptr);
+          bt->d_rowlen.ptr, bt->d_status.ptr, bt->d_lenord.ptr + ch.lo);
       TA_CK(cudaGetLastError());
       ++launches;
-      if (timed) {
-        TA_CK(cudaEventRecord(bt->evw1, st));
-        TA_CK(cudaEventSynchronize(bt->evw1));
-        TA_CK(cudaEventElapsedTime(&walker_ms, bt->evw0, bt->evw1));
+      if (timed) TA_CK(cudaEventRecord(bt->evw1, st));
+      if (scatter) {
+        // chunk c-1's rows were queued for copy behind its kernels: scatter
+        // them now (the GPU already has chunk c), then queue chunk c's copy
+        // into the slot chunk c-2 used (already scattered)
+        if (c > 0)
+          if (int rc = scatter_chunk(c - 1)) return rc;
+        TA_CK(cudaEventRecord(bt->evk[c & 1], st));
+        TA_CK(cudaStreamWaitEvent(ctx->d2h, bt->evk[c & 1], 0));
+        TA_CK(cudaMemcpyAsync(ctx->h_rows[c & 1].ptr, bt->d_rows.ptr + ch.rlo, size_t(ch.rhi - ch.rlo),
+                              cudaMemcpyDeviceToHost, ctx->d2h));
+        TA_CK(cudaMemcpyAsync(ctx->h_len[c & 1].ptr, bt->d_lenord.ptr + ch.lo, size_t(m) * 4, cudaMemcpyDeviceToHost,
+                              ctx->d2h));
+        TA_CK(cudaEventRecord(bt->evc[c & 1], ctx->d2h));
       }
     }
     TA_CK(cudaEventRecord(bt->ev1, st));
+    if (scatter && !chunks.empty())
+      if (int rc = scatter_chunk(chunks.size() - 1)) return rc;
     TA_CK(cudaEventSynchronize(bt->ev1));
     TA_CK(cudaEventElapsedTime(&ms_total, bt->ev0, bt->ev1));
+    if (chunks.size() == 1) TA_CK(cudaEventElapsedTime(&walker_ms, bt->evw0, bt->evw1));
     bt->stats.walker_ms = walker_ms;
+    bt->rows_scattered = scatter;
   }
   (void)rows_out;
   int64_t cells = 0;
@@ -1558,20 +1654,6 @@ void host_pack(const char* seqs, const int64_t* offs, int64_t lo, int64_t hi, co
   std::vector<std::thread> pool;
   for (int w = 0; w < nt; ++w) pool.emplace_back(work, lo + n * w / nt, lo + n * (w + 1) / nt);
   for (auto& th : pool) th.join();
-}
-
-// Host packing threads of one pipelined call: TA_HOST_THREADS if set (e.g.
-// cores / ranks when several processes share the host), else the cores
-// divided by the calls in flight in this process (run_batch runs one call
-// per worker thread and device), so concurrent workers do not oversubscribe.
-std::atomic<int> g_calls_in_flight{0};
-int host_threads() {
-  if (const char* e = std::getenv("TA_HOST_THREADS")) {
-    const int v = std::atoi(e);
-    if (v > 0) return v;
-  }
-  const int hw = int(std::max(1u, std::thread::hardware_concurrency()));
-  return std::max(1, hw / std::max(1, g_calls_in_flight.load()));
 }
 
 int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offsets, int64_t n,
@@ -2012,15 +2094,17 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
   TA_CK(cudaMemsetAsync(bt->d_begin.ptr, 0, nn * 12, st));
   TA_CK(cudaMemsetAsync(bt->d_status.ptr, 0, nn * 4, st));
   if (nn) TA_CK(cudaMemcpyAsync(bt->d_rowoff.ptr, roff.data(), nn * 8, cudaMemcpyHostToDevice, st));
+  bt->rows_scattered = false;
   if (int rc = run_impl(bt, *scheme, *opt, st, out)) return rc;
   ctx->last_stats = bt->stats;
   if (nn == 0) return TA_OK;
   std::vector<int32_t> dstat(nn), rlen(nn), beg(3 * nn);
-  std::vector<char> rows(size_t(total) + 1);
+  std::vector<char> rows(bt->rows_scattered ? 1 : size_t(total) + 1);
   TA_CK(cudaMemcpyAsync(dstat.data(), bt->d_status.ptr, nn * 4, cudaMemcpyDeviceToHost, st));
   TA_CK(cudaMemcpyAsync(rlen.data(), bt->d_rowlen.ptr, nn * 4, cudaMemcpyDeviceToHost, st));
   TA_CK(cudaMemcpyAsync(beg.data(), bt->d_begin.ptr, nn * 12, cudaMemcpyDeviceToHost, st));
-  TA_CK(cudaMemcpyAsync(rows.data(), bt->d_rows.ptr, size_t(total), cudaMemcpyDeviceToHost, st));
+  if (!bt->rows_scattered)
+    TA_CK(cudaMemcpyAsync(rows.data(), bt->d_rows.ptr, size_t(total), cudaMemcpyDeviceToHost, st));
   TA_CK(cudaStreamSynchronize(st));
   for (size_t t = 0; t < nn; ++t)
     if (bt->status[t] == TA_OK && dstat[t] != TA_OK) bt->status[t] = dstat[t];
@@ -2031,7 +2115,7 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
       for (int d = 0; d < 3; ++d) out->begins[3 * t + d] = ok ? beg[3 * t + d] : 0;
     }
     if (out->row_lens) out->row_lens[t] = ok ? rlen[t] : 0;
-    if (ok && out->rows0 && out->row_offsets) {
+    if (ok && out->rows0 && out->row_offsets && !bt->rows_scattered) {
       const int64_t cap = int64_t(bt->a[t]) + bt->b[t] + bt->c[t];
       const char* src = rows.data() + roff[t];
       std::memcpy(out->rows0 + out->row_offsets[t], src, size_t(rlen[t]));
