@@ -196,7 +196,8 @@ class Reference:
         if n < 0:
             raise RuntimeError(self.L.ref_last_error().decode())
         offs = np.ctypeslib.as_array(ctypes.cast(o, ctypes.POINTER(ctypes.c_int64)), shape=(3 * n + 1,)).copy()
-        seqs = np.frombuffer(ctypes.string_at(s, int(offs[-1])), np.uint8).copy()
+        # (string_at takes a C int: batches above 2 GiB, e.g. C3, need the array view)
+        seqs = np.ctypeslib.as_array(ctypes.cast(s, ctypes.POINTER(ctypes.c_uint8)), shape=(int(offs[-1]),)).copy()
         self.L.ref_free(s)
         self.L.ref_free(o)
         return seqs, offs
