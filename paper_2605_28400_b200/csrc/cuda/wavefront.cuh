@@ -302,6 +302,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   // bcnt counts threads that finished the item (the last one flushes).
   unsigned long long* const bkey = reinterpret_cast<unsigned long long*>(mbar + 2);     // [LANES][kSlots]
   uint32_t* const bcnt = reinterpret_cast<uint32_t*>(bkey + LANES * SM::kSlots);         // [LANES][kSlots]
+
   constexpr int GN = G * N;
 
   const int t = threadIdx.x;
@@ -346,6 +347,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
   // hot per-lane state in registers
   int si[LANES], la[LANES];
+  // semi: best M value of this tile's face row (0) / column (1) in the open
+  // item and where: slice * 16 + first maximal cell of the line (-1: none);
+  // offered once, when the item ends
+  [[maybe_unused]] int fbv[LANES][2], fbs[LANES][2];
+#pragma unroll
+  for (int l = 0; l < LANES; ++l) fbs[l][0] = fbs[l][1] = -1, fbv[l][0] = fbv[l][1] = INT_MIN;
   uint32_t s0word[LANES], flags[LANES];
 
   // 2-bit codes of the N bases at positions [pos, pos + N) of a sequence of
@@ -1014,50 +1021,58 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
         if constexpr (MODE == kSemi) {
           if (anyface) {
-            // faces j == b (tile row rb) and k == c (tile column cb)
+            // faces j == b (tile row rb) and k == c (tile column cb): per step
+            // only the line's maximum (in M units) is compared with the best
+            // of earlier slices (strictly greater: the earliest slice wins
+            // ties, oracle.cpp:74-85); the winning line is saved and its first
+            // maximal cell is resolved once, when the item ends
 #pragma unroll
             for (int l = 0; l < LANES; ++l) {
               if (!face[l]) continue;
               const int base = g2 * (si[l] + LS(l, kOrgJ) + LS(l, kOrgK) + j0 + k0);
               const int rbl = rb[l], cbl = cb[l];
-              const bool hasr = rbl < N, hasc = cbl < N;
-              // the face row (P = rb + 1) and column (Q = cb + 1) of the tile
-              uint32_t fr[N], fc[N];
-              if (hasr) select_row(rbl, fr);
-              if (hasc) select_col(cbl, fc);
-              int fm = INT_MIN;
-              if (hasr) {
+              if (rbl < N) {
+                uint32_t fr[N];
+                if (rbl == 0) {  // lengths that are multiples of N: no select
+#pragma unroll
+                  for (int Q = 1; Q <= N; ++Q) fr[Q - 1] = Cu[1][Q];
+                } else {
+                  select_row(rbl, fr);
+                }
                 uint32_t acc = fr[N - 1];
 #pragma unroll
                 for (int Q = N - 1; Q >= 1; --Q) acc = Ops::addmax(acc, g2s, fr[Q - 1]);
-                fm = (Ops::lane(acc, l) >> SH) + g2 * rbl;
+                const int hv = (Ops::lane(acc, l) >> SH) + g2 * rbl + base;
+                if (hv > fbv[l][0]) {
+                  int at = 0;
+#pragma unroll
+                  for (int x = N; x >= 1; --x)
+                    if ((Ops::lane(fr[x - 1], l) >> SH) + g2 * (rbl + x - 1) + base == hv) at = x;
+                  fbv[l][0] = hv;
+                  fbs[l][0] = si[l] * 16 + at;
+                }
               }
-              if (hasc) {
+              if (cbl < N) {
+                uint32_t fc[N];
+                if (cbl == 0) {
+#pragma unroll
+                  for (int P = 1; P <= N; ++P) fc[P - 1] = Cu[P][1];
+                } else {
+                  select_col(cbl, fc);
+                }
                 uint32_t acc = fc[N - 1];
 #pragma unroll
                 for (int P = N - 1; P >= 1; --P) acc = Ops::addmax(acc, g2s, fc[P - 1]);
-                fm = max(fm, (Ops::lane(acc, l) >> SH) + g2 * cbl);
-              }
-              if (!may_beat(l, fm + base)) continue;
-              int bv = 0, bp = 0, bq = 0;
-              bool have = false;
-              if (hasr) {
+                const int hv = (Ops::lane(acc, l) >> SH) + g2 * cbl + base;
+                if (hv > fbv[l][1]) {
+                  int at = 0;
 #pragma unroll
-                for (int Q = 1; Q <= N; ++Q) {
-                  const int v = (Ops::lane(fr[Q - 1], l) >> SH) + g2 * (rbl + Q - 1);
-                  if (!have || v > bv) bv = v, bq = Q, have = true;
-                }
-                bp = rbl + 1;
-              }
-              if (hasc) {
-#pragma unroll
-                for (int P = 1; P <= N; ++P) {
-                  const int v = (Ops::lane(fc[P - 1], l) >> SH) + g2 * (P - 1 + cbl);
-                  // row-major order between the two faces: smaller P first
-                  if (!have || v > bv || (v == bv && P < bp)) bv = v, bp = P, bq = cbl + 1, have = true;
+                  for (int x = N; x >= 1; --x)
+                    if ((Ops::lane(fc[x - 1], l) >> SH) + g2 * (cbl + x - 1) + base == hv) at = x;
+                  fbv[l][1] = hv;
+                  fbs[l][1] = si[l] * 16 + at;
                 }
               }
-              offer(l, bv + base, bp, bq);
             }
           }
         }
@@ -1082,6 +1097,23 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         si[l] += 1;
         sw[l] = BLOCKS ? si[l] >= LS(l, kLen) : si[l] > la[l];
         if (sw[l]) {
+          if constexpr (MODE == kSemi) {
+            // offer this tile's face bests of the finished item (one 64-bit key each)
+#pragma unroll
+            for (int f = 0; f < 2; ++f) {
+              if (fbs[l][f] < 0) continue;
+              const int oj = LS(l, kOrgJ), ok = LS(l, kOrgK);
+              const int line = f ? LS(l, kLenC) - ok - k0 : LS(l, kLenB) - oj - j0;  // rb or cb
+              const int sl = fbs[l][f] >> 4, at = fbs[l][f] & 15;
+              const uint32_t j = oj + j0 + (f ? at - 1 : line), k = ok + k0 + (f ? line : at - 1);
+              const unsigned long long lin =
+                  (static_cast<unsigned long long>(static_cast<uint32_t>(sl)) * static_cast<uint32_t>(LS(l, kLenB) + 1) + j) *
+                      static_cast<uint32_t>(LS(l, kLenC) + 1) + k;
+              atomicMax(args.out_key + LS(l, kTid), best_key(fbv[l][f], lin));
+              fbs[l][f] = -1;
+              fbv[l][f] = INT_MIN;
+            }
+          }
           if constexpr (MODE != kGlobal) {
             // the last thread to leave the item publishes its best and frees the slot
             const int slot = l * SM::kSlots + (LS(l, kItem) & (SM::kSlots - 1));
