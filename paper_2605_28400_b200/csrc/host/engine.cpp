@@ -1,3 +1,6 @@
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // Engine entry points over the C-ABI (reference: proj/src/tiled.cpp:8-98,
 // proj/src/oracle.cpp:182-190, proj/src/metrics.cpp:11-14).  Every alignment
 // is computed by the sm_100a kernels; error classes and messages follow the
@@ -139,7 +142,11 @@ BatchOut run_engine(const std::vector<const Triplet*>& ts, const ScoringScheme& 
     res.row_offsets = out.row_off.data();
     res.row_lens = out.row_len.data();
   }
+  const auto t0 = std::chrono::steady_clock::now();
   const int rc = ta_align_batch(device, seqs.data(), offs.data(), int64_t(n), &sch, &opt, &res, nullptr);
+  if (std::getenv("TA_PROFILE_CLI"))
+    std::fprintf(stderr, "[engine] ta_align_batch %.1f ms (%zu triplets)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), n);
   if (rc != TA_OK) throw_status(rc, ta_last_error());
   return out;
 }
