@@ -527,9 +527,10 @@ def main(argv=None):
     rows = None
     if not args.no_rows and rank == 0 and world == 1:
         rcases, c1 = measure_rows(ta, local, sh, args.rows_c2)
-        rows = {"cases": rcases, "algorithmic_dir_bytes_per_cell": 0.5,
-                "note": "direction records: 4-bit codes per swept cell, 64 B per 100-cell tile-slice; "
-                        "e2e = align_arrays(with_rows) from host ASCII to host row planes"}
+        rows = {"cases": rcases, "algorithmic_dir_bytes_per_cell": 0.375,
+                "note": "direction records: 3-bit codes per swept cell (algorithmic 0.375 B/cell), stored as "
+                        "40 B per 100-cell tile-slice and lane; dir_bytes_per_cell counts swept (padded) cells "
+                        "against real cells; e2e = align_arrays(with_rows) from host ASCII to host row planes"}
         if not args.no_cpu_baseline:
             try:
                 rcpu, ref = rows_cpu_baseline(*c1, ROWS_CPU_SAMPLE)
