@@ -132,7 +132,7 @@ def maybe_relaunch(args, argv):
     if not args.dry_run:
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("TA_BENCH_SHARE_GPU") != "1":
             print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {have} GPU(s) visible"}))
             return 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
@@ -400,13 +400,18 @@ def main(argv=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TA_BENCH_SHARE_GPU=1 (test only): ranks share the visible GPUs round robin
+    # and reduce over gloo, so the multi-rank path runs on a one-GPU box
+    share = os.environ.get("TA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = local % max(1, torch.cuda.device_count())
     if torch.cuda.device_count() <= local:
         raise SystemExit(f"rank {rank}: LOCAL_RANK {local} but {torch.cuda.device_count()} GPU(s) visible")
     local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
     # host pack threads of the e2e pipeline: the host's cores shared by the ranks
     os.environ.setdefault("TA_HOST_THREADS", str(max(1, (os.cpu_count() or 1) // max(1, local_world))))
     torch.cuda.set_device(local)
-    d = Dist(world, local, "nccl")
+    d = Dist(world, local, "gloo" if share else "nccl")
 
     w = WORKLOADS[args.workload]
     spec_all, lo, hi, total = rank_plan(args, rank, world)
