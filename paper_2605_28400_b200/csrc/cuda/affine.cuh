@@ -76,10 +76,13 @@ template <int N, int G, int LANES, int BLK>
 struct AffSmem {
   static constexpr int T = G * G;
   static constexpr int NN = N * N;
-  static constexpr int XW = 8 * N;
+  // mailbox slot per tile: the right column as (B, E3, E4, E7) per row, then
+  // the bottom row as (B, E4, E2, E6) per column (one 16-byte vector per
+  // position), padded to 11 vectors so 8 consecutive slots hit distinct banks
+  static constexpr int XW = 8 * N + 4;  // 2N + 1 vectors (odd: 8 consecutive slots are bank-conflict free)
   static constexpr size_t kSig = size_t(NN) * T * 4;
   static constexpr size_t kTab = size_t(N) * T * 8;
-  static constexpr size_t kX = (size_t(2) * XW * (T + 1) * 4 + 15) / 16 * 16;
+  static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
   static constexpr int kLaneFields = 12;
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
   // prefetched faces: int4 per position (sequential blocks) or tagged ring
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   uint32_t* const s12w = reinterpret_cast<uint32_t*>(smem_raw);  // [NN][T]
   unsigned char* const tab1 = smem_raw + SM::kSig;
   unsigned char* const tab2 = tab1 + SM::kTab;
-  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);  // [2][XW][T+1]
+  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);  // [2][T+1][XW]
   int32_t* const lst = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX);
   int32_t* const stage = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX + SM::kLane);  // [LANES][2G][N+1][4]
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(tab2 + SM::kTab + SM::kX + SM::kLane + SM::kStage);
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
                                     : static_cast<uint32_t>(2 * args.open * SC);
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
-  for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
+  for (int w = t; w < 2 * XW; w += T) xbuf[((w / XW) * (T + 1) + T) * XW + w % XW] = NEG;
   for (int w = t; w < LANES * SM::kSlots; w += T) {
     bkey[w] = 0ull;
     bcnt[w] = 0u;
@@ -308,20 +311,22 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           cE6[N + 1][N + 1], cE7[N + 1][N + 1];
       uint32_t rec[TRACE ? NN : 1];
       // ---- 1. halos of this slice (published by the neighbours at step s-1)
-      const uint32_t* xin = xbuf + (buf ^ 1) * XW * (T + 1);
+      const uint4* xin = reinterpret_cast<const uint4*>(xbuf + (buf ^ 1) * XW * (T + 1));
 #pragma unroll
       for (int q = 0; q < N; ++q) {
-        cB[0][q] = xin[(4 * N + q) * (T + 1) + up];
-        cE4[0][q] = xin[(5 * N + q) * (T + 1) + up];
-        cE2[0][q + 1] = xin[(6 * N + q) * (T + 1) + up];
-        cE6[0][q + 1] = xin[(7 * N + q) * (T + 1) + up];
+        const uint4 v = xin[up * (XW / 4) + N + q];
+        cB[0][q] = v.x;
+        cE4[0][q] = v.y;
+        cE2[0][q + 1] = v.z;
+        cE6[0][q + 1] = v.w;
       }
 #pragma unroll
       for (int p = 0; p < N; ++p) {
-        cB[p + 1][0] = xin[p * (T + 1) + left];
-        cE3[p + 1][0] = xin[(N + p) * (T + 1) + left];
-        cE4[p + 1][0] = xin[(2 * N + p) * (T + 1) + left];
-        cE7[p + 1][0] = xin[(3 * N + p) * (T + 1) + left];
+        const uint4 v = xin[left * (XW / 4) + p];
+        cB[p + 1][0] = v.x;
+        cE3[p + 1][0] = v.y;
+        cE4[p + 1][0] = v.z;
+        cE7[p + 1][0] = v.w;
       }
       if (BLOCKS && (r == 0 || cc == 0)) {
         bool top = false, lft = false;
@@ -551,21 +556,11 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       sweep();
 
       // ---- 5. publish right column / bottom row -----------------------------
-      uint32_t* xout = xbuf + buf * XW * (T + 1) + tile;
+      uint4* xout = reinterpret_cast<uint4*>(xbuf + buf * XW * (T + 1)) + tile * (XW / 4);
 #pragma unroll
-      for (int p = 0; p < N; ++p) {
-        xout[p * (T + 1)] = cB[p + 1][N];
-        xout[(N + p) * (T + 1)] = cE3[p + 1][N];
-        xout[(2 * N + p) * (T + 1)] = cE4[p + 1][N];
-        xout[(3 * N + p) * (T + 1)] = cE7[p + 1][N];
-      }
+      for (int p = 0; p < N; ++p) xout[p] = make_uint4(cB[p + 1][N], cE3[p + 1][N], cE4[p + 1][N], cE7[p + 1][N]);
 #pragma unroll
-      for (int q = 0; q < N; ++q) {
-        xout[(4 * N + q) * (T + 1)] = cB[N][q];
-        xout[(5 * N + q) * (T + 1)] = cE4[N][q];
-        xout[(6 * N + q) * (T + 1)] = cE2[N][q + 1];
-        xout[(7 * N + q) * (T + 1)] = cE6[N][q + 1];
-      }
+      for (int q = 0; q < N; ++q) xout[N + q] = make_uint4(cB[N][q], cE4[N][q], cE2[N][q + 1], cE6[N][q + 1]);
       if (BLOCKS && (r == G - 1 || cc == G - 1)) {
         bool wrote = false;
 #pragma unroll
