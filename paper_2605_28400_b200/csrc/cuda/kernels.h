@@ -50,7 +50,7 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
 }  // namespace ta
 
 #define TA_KERNEL_ENTRY(G, L, M, TR, BL) \
-  KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR, BL>, WaveSmem<kTileN, G, L>::bytes, G * G, G}
+  KernelEntry{&wavefront_kernel<kTileN, G, L, M, TR, BL>, WaveSmem<kTileN, G, L, BL>::bytes, G * G, G}
 
 #define TA_DEFINE_KERNEL_TABLE(G, WITH_BLOCKS)                                         \
   namespace ta {                                                                       \
@@ -103,15 +103,15 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
     constexpr int N8 = kSmallTileN;                                                                \
     if (lanes == 1) {                                                                              \
       switch (mode) {                                                                              \
-        case kGlobal: return {&wavefront_kernel<N8, 16, 1, kGlobal, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16}; \
-        case kSemi: return {&wavefront_kernel<N8, 16, 1, kSemi, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16};     \
-        case kLocal: return {&wavefront_kernel<N8, 16, 1, kLocal, false, 1>, WaveSmem<N8, 16, 1>::bytes, 256, 16};   \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 1, kGlobal, false, 1>, WaveSmem<N8, 16, 1, 1>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 1, kSemi, false, 1>, WaveSmem<N8, 16, 1, 1>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 1, kLocal, false, 1>, WaveSmem<N8, 16, 1, 1>::bytes, 256, 16};   \
       }                                                                                            \
     } else {                                                                                       \
       switch (mode) {                                                                              \
-        case kGlobal: return {&wavefront_kernel<N8, 16, 2, kGlobal, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16}; \
-        case kSemi: return {&wavefront_kernel<N8, 16, 2, kSemi, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16};     \
-        case kLocal: return {&wavefront_kernel<N8, 16, 2, kLocal, false, 1>, WaveSmem<N8, 16, 2>::bytes, 256, 16};   \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 2, kGlobal, false, 1>, WaveSmem<N8, 16, 2, 1>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 2, kSemi, false, 1>, WaveSmem<N8, 16, 2, 1>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 2, kLocal, false, 1>, WaveSmem<N8, 16, 2, 1>::bytes, 256, 16};   \
       }                                                                                            \
     }                                                                                              \
     return {};                                                                                     \

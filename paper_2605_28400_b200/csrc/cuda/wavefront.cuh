@@ -245,17 +245,25 @@ __device__ __forceinline__ int base_at(const uint32_t* __restrict__ seq, uint32_
   return static_cast<int>((__ldg(seq + w + (pos >> 4)) >> ((pos & 15) * 2)) & 3u);
 }
 
-template <int N, int G, int LANES>
+template <int N, int G, int LANES, int BLK = 1>
 struct WaveSmem {
   static constexpr int T = G * G;
   static constexpr int NN = N * N;
-  static constexpr int XW = 2 * N + 1;
+  // Mailbox slot per tile: the down row (N + 1 values incl. the corner) at
+  // words [0, DR), the right column (N values) at [DR, DR + RC), 16-byte
+  // aligned for vector loads / stores; an odd number of vectors per slot
+  // keeps 8 consecutive slots (one LDS.128 phase) on distinct banks.
+  static constexpr int DR = (N + 1 + 3) / 4 * 4;
+  static constexpr int RC = (N + 3) / 4 * 4;
+  static constexpr int XV = ((DR + RC) / 4) % 2 ? (DR + RC) / 4 : (DR + RC) / 4 + 1;  // vectors per slot
+  static constexpr int XW = 4 * XV;
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
-  static constexpr size_t kX = (size_t(2) * XW * (T + 1) * 4 + 15) / 16 * 16;
-  static constexpr int kLaneFields = 12;                   // cold per-lane state
+  static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
+  static constexpr int kLaneFields = 10;                   // cold per-lane state
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
-  static constexpr size_t kStage = size_t(LANES) * 2 * G * kSegE * 8;  // prefetched block faces (either layout)
+  // prefetched block faces (either layout); single-plane kernels have none
+  static constexpr size_t kStage = BLK ? size_t(LANES) * 2 * G * kSegE * 8 : 0;
   static constexpr size_t kBar = 16;                       // two mbarriers (mailbox parity)
   static constexpr int kSlots = 64;                        // open stream items per lane (ring)
   static constexpr size_t kBest = size_t(LANES) * kSlots * 12;  // per-item best key + finish count
@@ -264,7 +272,7 @@ struct WaveSmem {
 
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kUnused6, kUnused7, kOrgJ, kOrgK, kLen, kBk };
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk };
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
@@ -278,7 +286,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   static_assert((N * N) % 4 == 0, "tile cells must group by 4");
   static_assert(!TRACE || N * N == 10 * kDirWords, "direction records hold 10 cells per word");
   using Ops = LaneOps<LANES>;
-  using SM = WaveSmem<N, G, LANES>;
+  using SM = WaveSmem<N, G, LANES, BLK>;
   constexpr int T = SM::T;
   [[maybe_unused]] constexpr int NN = SM::NN;
   constexpr int XW = SM::XW;
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   uint32_t* const s12w = reinterpret_cast<uint32_t*>(smem_raw);
   unsigned char* const tab1 = smem_raw + SM::kSig;                            // 8 B per (row, thread)
   unsigned char* const tab2 = tab1 + SM::kTab;
-  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);        // [2][XW][T+1]
+  uint32_t* const xbuf = reinterpret_cast<uint32_t*>(tab2 + SM::kTab);        // [2][T+1][XW]
   int32_t* const lst = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX);  // [LANES][8][T]
   int32_t* const stage = reinterpret_cast<int32_t*>(tab2 + SM::kTab + SM::kX + SM::kLane);  // [LANES][2G][N+1]
   uint64_t* const mbar = reinterpret_cast<uint64_t*>(tab2 + SM::kTab + SM::kX + SM::kLane + SM::kStage);
@@ -335,7 +343,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   [[maybe_unused]] const uint32_t pw[5] = {one, one << 3, one << 6, one << 9, one << 12};
   auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
 
-  for (int w = t; w < 2 * XW; w += T) xbuf[w * (T + 1) + T] = NEG;
+  for (int w = t; w < 2 * XW; w += T) xbuf[((w / XW) * (T + 1) + T) * XW + w % XW] = NEG;
   for (int w = t; w < LANES * SM::kSlots; w += T) {
     bkey[w] = 0ull;
     bcnt[w] = 0u;
@@ -591,11 +599,32 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
      if (work) {
       uint32_t Cu[N + 1][N + 1];
       // ---- 1. new halos (published by the neighbours at step s-1) --------
-      const uint32_t* xin = xbuf + (buf ^ 1) * XW * (T + 1);
+      {
+        const uint4* xu = reinterpret_cast<const uint4*>(xbuf + ((buf ^ 1) * (T + 1) + up) * XW);
+        const uint4* xl = reinterpret_cast<const uint4*>(xbuf + ((buf ^ 1) * (T + 1) + left) * XW + SM::DR);
 #pragma unroll
-      for (int q = 0; q <= N; ++q) Cu[0][q] = xin[(N + q) * (T + 1) + up];
+        for (int v = 0; v < SM::DR / 4; ++v) {
+          const uint4 e = xu[v];
+          const uint32_t w4[4] = {e.x, e.y, e.z, e.w};
 #pragma unroll
-      for (int p = 0; p < N; ++p) Cu[p + 1][0] = xin[p * (T + 1) + left];
+          for (int u = 0; u < 4; ++u)
+            if (4 * v + u <= N) Cu[0][4 * v + u] = w4[u];
+        }
+#pragma unroll
+        for (int v = 0; v < SM::RC / 4; ++v) {
+          if (4 * v + 2 >= N) {  // the last pair (N % 4 == 2): one 8-byte load
+            const uint2 e = reinterpret_cast<const uint2*>(xl + v)[0];
+            Cu[4 * v + 1][0] = e.x;
+            if (4 * v + 1 < N) Cu[4 * v + 2][0] = e.y;
+            continue;
+          }
+          const uint4 e = xl[v];
+          const uint32_t w4[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (4 * v + u < N) Cu[4 * v + u + 1][0] = w4[u];
+        }
+      }
       if (BLOCKS && (r == 0 || cc == 0)) {
         bool top = false, lft = false;
 #pragma unroll
@@ -849,11 +878,27 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       sweep_tile();
 
       // ---- 5. publish right column / down row (+ corner) ----------------
-      uint32_t* xout = xbuf + buf * XW * (T + 1) + tile;
+      {
+        uint4* xo = reinterpret_cast<uint4*>(xbuf + (buf * (T + 1) + tile) * XW);
 #pragma unroll
-      for (int p = 0; p < N; ++p) xout[p * (T + 1)] = Cu[p + 1][N];
+        for (int v = 0; v < SM::DR / 4; ++v) {
+          uint32_t w4[4];
 #pragma unroll
-      for (int q = 0; q <= N; ++q) xout[(N + q) * (T + 1)] = Cu[N][q];
+          for (int u = 0; u < 4; ++u) w4[u] = 4 * v + u <= N ? Cu[N][4 * v + u] : 0u;
+          xo[v] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+#pragma unroll
+        for (int v = 0; v < SM::RC / 4; ++v) {
+          uint32_t w4[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) w4[u] = 4 * v + u < N ? Cu[4 * v + u + 1][N] : 0u;
+          if (4 * v + 2 >= N) {
+            reinterpret_cast<uint2*>(xo + SM::DR / 4 + v)[0] = make_uint2(w4[0], w4[1]);
+          } else {
+            xo[SM::DR / 4 + v] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+          }
+        }
+      }
       if (BLOCKS && (r == G - 1 || cc == G - 1)) {
         bool wrote = false;
 #pragma unroll
