@@ -220,6 +220,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     LS(l, kOrgK) = K * GN;
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
+    LS(l, kBj) = Bj;
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
     uint32_t f = (id >= 0 || (WAVE && it < iend)) ? 0u : kDone;
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
@@ -288,6 +289,24 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     s0word[l] = 0;
     tables_lane(l, fetch(l, it, ie));
   }
+  // Paired lanes (sequential block items only): both lanes hold block items of
+  // identical geometry in lockstep (the host pairs equal-shape triplets), so
+  // their block faces travel as packed s16x2 words through lane 0's face
+  // buffer: one store / prefetch / load per position instead of a per-lane
+  // extract, splat and masked merge.  Holds for all blocks of a triplet pair.
+  constexpr bool kPackFaces = LANES == 2 && BLK == 1;
+  auto lockstep = [&]() -> bool {
+    if constexpr (!kPackFaces) {
+      return false;
+    } else {
+      return !(flags[0] & kDone) && !(flags[1] & kDone) && LS(0, kTid) >= 0 && LS(1, kTid) >= 0 &&
+             // same slices and block grid: every later block of the two
+             // triplets lines up too, so producer and consumer agree on the packing
+             si[0] == si[1] && la[0] == la[1] && LS(0, kBj) == LS(1, kBj) && LS(0, kBk) == LS(1, kBk) &&
+             LS(0, kOrgJ) == LS(1, kOrgJ) && LS(0, kOrgK) == LS(1, kOrgK) && LS(0, kLen) == LS(1, kLen);
+    }
+  };
+  bool paired = lockstep();
 
   // previous-slice state (incl. the halo row / column received last step)
   uint32_t pB[N + 1][N + 1], pE2[N + 1][N + 1], pE3[N + 1][N + 1], pE5[N + 1][N + 1];
@@ -337,6 +356,34 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         }
         if (top || lft) {
           asm volatile("cp.async.wait_all;" ::: "memory");
+          if (kPackFaces && paired) {
+            if (r == 0 && (flags[0] & kInTop) && si[0] <= la[0]) {
+              const uint4* st = reinterpret_cast<const uint4*>(stage) + cc * (N + 1);
+#pragma unroll
+              for (int q = 0; q <= N; ++q) {
+                const uint4 v = st[q];  // packed (B, E2, E4, E6) at k = cN + q - 1
+                if (q < N) {
+                  cB[0][q] = v.x;
+                  cE4[0][q] = v.z;
+                }
+                if (q > 0) {
+                  cE2[0][q] = v.y;
+                  cE6[0][q] = v.w;
+                }
+              }
+            }
+            if (cc == 0 && (flags[0] & kInLeft) && si[0] <= la[0]) {
+              const uint4* st = reinterpret_cast<const uint4*>(stage) + (G + r) * (N + 1);
+#pragma unroll
+              for (int p = 0; p < N; ++p) {
+                const uint4 v = st[p];  // packed (B, E3, E4, E7) at j = rN + p
+                cB[p + 1][0] = v.x;
+                cE3[p + 1][0] = v.y;
+                cE4[p + 1][0] = v.z;
+                cE7[p + 1][0] = v.w;
+              }
+            }
+          } else
 #pragma unroll
           for (int l = 0; l < LANES; ++l) {
             const bool ok = si[l] <= la[l];
@@ -599,6 +646,23 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             }
             continue;
           }
+          if (kPackFaces && paired) {  // lane 0's buffer, both lanes packed; once
+            if (l != 0) continue;
+            uint4* fb = reinterpret_cast<uint4*>(args.faces + args.face_off[sbase]);
+            if (dn) {
+              uint4* d = fb + (int64_t(LS(0, kOrgK) / GN) * a1 + si[0]) * (GN + 1) + cc * N;
+              if (cc == 0) d[0] = make_uint4(cB[N][0], 0u, cE4[N][0], 0u);
+#pragma unroll
+              for (int q = 1; q <= N; ++q) d[q] = make_uint4(cB[N][q], cE2[N][q], cE4[N][q], cE6[N][q]);
+            }
+            if (rt) {
+              uint4* d = fb + int64_t(LS(0, kBk)) * a1 * (GN + 1) + int64_t(si[0]) * GN + r * N;
+#pragma unroll
+              for (int p = 0; p < N; ++p) d[p] = make_uint4(cB[p + 1][N], cE3[p + 1][N], cE4[p + 1][N], cE7[p + 1][N]);
+            }
+            wrote = true;
+            continue;
+          }
           int4* fb = reinterpret_cast<int4*>(args.faces + args.face_off[sbase + l]);
           if (dn) {  // own cells Q = 1..N at positions cN + Q; tile 0 also the corner (its halo)
             int4* d = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
@@ -795,6 +859,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         }
 
       // ---- 9. advance the lanes ---------------------------------------------------
+      [[maybe_unused]] bool switched = false;
 #pragma unroll
       for (int l = 0; l < LANES; ++l) {
         if (flags[l] & kDone) continue;
@@ -815,6 +880,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         LS(l, kItem) = it;
         tables_lane(l, fetch(l, it, LS(l, kIEnd)));
         si[l] = 0;
+        switched = true;
 #pragma unroll
         for (int P = 0; P <= N; ++P)
 #pragma unroll
@@ -825,6 +891,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             pE5[P][Q] = lop_sel(pE5[P][Q], NEG, Ops::mask(l));
           }
       }
+      if (kPackFaces && switched) paired = lockstep();
     } else {
       mbar_arrive_group(&mbar[buf]);
     }
@@ -861,6 +928,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             fetch_seg(G + r, fw + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kAffSegE);
           continue;
         }
+        if (kPackFaces && paired && l != 0) continue;  // packed faces: lane 0's buffer only
         const int4* fb = reinterpret_cast<const int4*>(args.faces + args.face_off[sbase + l]);
         if (r == 0 && (flags[l] & kInTop)) {
           const int4* src = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;

@@ -272,7 +272,7 @@ struct WaveSmem {
 
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk };
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk, kBj };  // kBj: affine only
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>

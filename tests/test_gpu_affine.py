@@ -184,3 +184,19 @@ def test_affine_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
             want = oracle.affine(t, sch, mode)
             assert int(out["status"][x]) == 0
             assert int(out["score"][x]) == want["score"] and list(out["end"][x]) == want["end"], (sch, mode, x)
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_open_zero_equals_linear_on_mixed_block_grids(gpu_engine, mode):
+    """Mixed lengths (C4-like, 64-512 bp): paired lanes whose first blocks
+    look alike but whose block grids differ must not share packed faces.  With
+    gap_open = 0 the forced affine kernels equal the linear kernels exactly."""
+    ta = gpu_engine
+    seqs, offs = ta.generate("uniform:64:512:3000", 0.08, 0.01, 4)
+    lin = ta.align_arrays(seqs, offs, ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(mode),
+                          cfg=ta.EngineConfig(cell_budget=1 << 40))
+    aff = ta.align_arrays(seqs, offs, ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(mode),
+                          cfg=ta.EngineConfig(cell_budget=1 << 40, gap_model=1))
+    assert (lin["status"] == 0).all() and (aff["status"] == 0).all()
+    bad = np.flatnonzero((lin["score"] != aff["score"]) | (lin["end"] != aff["end"]).any(axis=1))
+    assert len(bad) == 0, bad[:10].tolist()
