@@ -260,7 +260,7 @@ struct WaveSmem {
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
   static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
-  static constexpr int kLaneFields = 10;                   // cold per-lane state
+  static constexpr int kLaneFields = 11;                   // cold per-lane state
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
   // prefetched block faces (either layout); single-plane kernels have none
   static constexpr size_t kStage = BLK ? size_t(LANES) * 2 * G * kSegE * 8 : 0;
@@ -272,7 +272,7 @@ struct WaveSmem {
 
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk, kBj };  // kBj: affine only
+enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk, kBj };
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
@@ -424,6 +424,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kOrgK) = K * GN;
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
+    LS(l, kBj) = Bj;
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
     uint32_t f = (id >= 0 || it < iend) ? 0u : kDone;  // a null item keeps the lane alive
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
@@ -556,6 +557,22 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   } else {
     tables_lane(0, first[0]);
   }
+  // Paired lanes (sequential block items): both lanes hold block items with the
+  // same slices and block grid in lockstep (the host pairs equal-shape
+  // triplets), so their block faces travel as packed words through lane 0's
+  // face buffer: one store / prefetch / load per position instead of a
+  // per-lane extract, splat and masked merge (see affine.cuh).
+  constexpr bool kPackFaces = LANES == 2 && BLK == 1;
+  auto lockstep = [&]() -> bool {
+    if constexpr (!kPackFaces) {
+      return false;
+    } else {
+      return !(flags[0] & kDone) && !(flags[1] & kDone) && LS(0, kTid) >= 0 && LS(1, kTid) >= 0 &&
+             si[0] == si[1] && la[0] == la[1] && LS(0, kBj) == LS(1, kBj) && LS(0, kBk) == LS(1, kBk) &&
+             LS(0, kOrgJ) == LS(1, kOrgJ) && LS(0, kOrgK) == LS(1, kOrgK) && LS(0, kLen) == LS(1, kLen);
+    }
+  };
+  bool paired = lockstep();
 
   uint32_t Pv[N + 1][N + 1];
 #pragma unroll
@@ -634,6 +651,18 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
         if (top || lft) {
           asm volatile("cp.async.wait_all;" ::: "memory");
+          if (kPackFaces && paired) {
+            if (r == 0 && (flags[0] & kInTop) && si[0] <= la[0]) {
+              const uint32_t* st = reinterpret_cast<const uint32_t*>(stage) + cc * (N + 1);
+#pragma unroll
+              for (int q = 0; q <= N; ++q) Cu[0][q] = st[q];
+            }
+            if (cc == 0 && (flags[0] & kInLeft) && si[0] <= la[0]) {
+              const uint32_t* st = reinterpret_cast<const uint32_t*>(stage) + (G + r) * (N + 1);
+#pragma unroll
+              for (int p = 0; p < N; ++p) Cu[p + 1][0] = st[p];
+            }
+          } else
 #pragma unroll
           for (int l = 0; l < LANES; ++l) {
             const bool ok = si[l] <= la[l];
@@ -924,6 +953,22 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             }
             continue;
           }
+          if (kPackFaces && paired) {  // lane 0's buffer, both lanes packed; once
+            if (l != 0) continue;
+            uint32_t* fb = reinterpret_cast<uint32_t*>(args.faces + args.face_off[sbase]);
+            if (dn) {
+              uint32_t* d = fb + (int64_t(LS(0, kOrgK) / GN) * a1 + si[0]) * (GN + 1) + cc * N;
+#pragma unroll
+              for (int q = 0; q <= N; ++q) d[q] = Cu[N][q];
+            }
+            if (rt) {
+              uint32_t* d = fb + int64_t(LS(0, kBk)) * a1 * (GN + 1) + int64_t(si[0]) * GN + r * N;
+#pragma unroll
+              for (int p = 0; p < N; ++p) d[p] = Cu[p + 1][N];
+            }
+            wrote = true;
+            continue;
+          }
           int32_t* fb = args.faces + args.face_off[sbase + l];
           if (dn) {  // Fdown[K][i][cN + q], q = 0 is the corner (k = cN - 1)
             int32_t* d = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;
@@ -1186,7 +1231,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         for (int P = 0; P <= N; ++P)
 #pragma unroll
           for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = NEG;
+        if constexpr (kPackFaces) paired = lockstep();
       } else {
+        [[maybe_unused]] bool switched = false;
 #pragma unroll
         for (int l = 0; l < LANES; ++l) {
           if (!sw[l]) continue;
@@ -1194,11 +1241,13 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           LS(l, kItem) = it;
           setup(l, it, LS(l, kIEnd));
           si[l] = 0;
+          switched = true;
 #pragma unroll
           for (int P = 0; P <= N; ++P)
 #pragma unroll
             for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = lop_sel(Pv[P][Q], NEG, Ops::mask(l));
         }
+        if (kPackFaces && switched) paired = lockstep();
       }
     } else {
       mbar_arrive_group(&mbar[buf]);
@@ -1236,6 +1285,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             fetch_seg(G + r, fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
           continue;
         }
+        if (kPackFaces && paired && l != 0) continue;  // packed faces: lane 0's buffer only
         const int32_t* fb = args.faces + args.face_off[sbase + l];
         if (r == 0 && (flags[l] & kInTop)) {
           const int32_t* src = fb + (int64_t(LS(l, kOrgK) / GN) * a1 + si[l]) * (GN + 1) + cc * N;

@@ -3,7 +3,7 @@
 C4 prefix), kernel time from the engine's CUDA events, best of 3; prints one
 JSON line per case with a result checksum.  TA_LIB_PATH_EXPERIMENT selects a
 variant build of the same ABI.
-usage: ab_quick.py [--n 200000] [--c4 0] [--modes 0,1,2] [--gap-open 0]"""
+usage: ab_quick.py [--n 200000] [--c4 0] [--c3 0] [--modes 0,1,2] [--gap-open 0]"""
 import argparse
 import json
 import os
@@ -17,6 +17,7 @@ import paper_2605_28400_b200 as ta  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=200000)
 ap.add_argument("--c4", type=int, default=0)
+ap.add_argument("--c3", type=int, default=0)
 ap.add_argument("--modes", default="0,1,2")
 ap.add_argument("--gap-open", type=int, default=0)
 args = ap.parse_args()
@@ -24,6 +25,8 @@ sch = ta.ScoringScheme(1, -1, -2, args.gap_open)
 cases = [("C2", f"fixed:150:150:150:{args.n}", 0.025, 0.005, 2)]
 if args.c4:
     cases.append(("C4", f"uniform:64:512:{args.c4}", 0.08, 0.01, 4))
+if args.c3:
+    cases.append(("C3", f"fixed:250:250:250:{args.c3}", 0.025, 0.005, 3))
 lib = os.environ.get("TA_LIB_PATH_EXPERIMENT", "in-tree")
 for name, spec, mut, ind, seed in cases:
     seqs, offs = ta.generate(spec, mut, ind, seed)
