@@ -249,30 +249,44 @@ template <int N, int G, int LANES, int BLK = 1>
 struct WaveSmem {
   static constexpr int T = G * G;
   static constexpr int NN = N * N;
+  // Pipeline lag: tile (r, c) runs stream position s - LAG (r + c) at step s,
+  // so the halos it reads at step s were published LAG steps earlier.  With
+  // LAG = 2 (single-plane kernels) a warp waits only for step s - 2 before it
+  // reads and for step s - 1 before it overwrites a mailbox buffer (NB = 3):
+  // warps drift up to one step apart instead of meeting at every step, so the
+  // tail of one warp's step overlaps the start of the next step of the others.
+  // Block kernels keep LAG = 1 (their face timing is derived for it).
+  static constexpr int LAG = BLK == 0 ? 2 : 1;
+  static constexpr int NB = LAG + 1;  // mailbox buffers
   // Mailbox slot per tile: the down row (N + 1 values incl. the corner) at
   // words [0, DR), the right column (N values) at [DR, DR + RC), 16-byte
-  // aligned for vector loads / stores; an odd number of vectors per slot
-  // keeps 8 consecutive slots (one LDS.128 phase) on distinct banks.
+  // aligned for vector loads / stores; with two buffers an odd number of
+  // vectors per slot keeps 8 slots of one LDS.128 phase on distinct banks
+  // (three buffers do not fit with the padding: 2-way conflicts instead).
   static constexpr int DR = (N + 1 + 3) / 4 * 4;
   static constexpr int RC = (N + 3) / 4 * 4;
-  static constexpr int XV = ((DR + RC) / 4) % 2 ? (DR + RC) / 4 : (DR + RC) / 4 + 1;  // vectors per slot
+  static constexpr int XV = (((DR + RC) / 4) % 2 || NB > 2) ? (DR + RC) / 4 : (DR + RC) / 4 + 1;  // vectors per slot
   static constexpr int XW = 4 * XV;
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
-  static constexpr size_t kX = size_t(2) * XW * (T + 1) * 4;
-  static constexpr int kLaneFields = 11;                   // cold per-lane state
+  static constexpr size_t kX = size_t(NB) * XW * (T + 1) * 4;
+  // cold per-lane state: single-plane kernels keep no block geometry
+  static constexpr int kLaneFields = BLK ? 10 : 6;
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
   // prefetched block faces (either layout); single-plane kernels have none
   static constexpr size_t kStage = BLK ? size_t(LANES) * 2 * G * kSegE * 8 : 0;
-  static constexpr size_t kBar = 16;                       // two mbarriers (mailbox parity)
+  static constexpr size_t kBar = 48;                       // NB <= 4 mbarriers + per-lane stream ends
   static constexpr int kSlots = 64;                        // open stream items per lane (ring)
   static constexpr size_t kBest = size_t(LANES) * kSlots * 12;  // per-item best key + finish count
   static constexpr size_t bytes = kSig + 2 * kTab + kX + kLane + kStage + kBar + kBest;
+  static_assert(bytes <= 232448, "shared memory");
+  static_assert(kSlots > 2 * LAG * (G - 1), "open items per lane exceed the ring");
 };
 
 
-// Cold per-lane fields kept in shared memory ([lane][field][thread]).
-enum LaneField { kItem = 0, kIEnd, kTid, kLenB, kLenC, kW0, kOrgJ, kOrgK, kLen, kBk, kBj };
+// Cold per-lane fields kept in shared memory ([lane][field][thread]); the
+// block geometry (kOrgJ ..) is stored by block kernels only (constants else).
+enum LaneField { kItem = 0, kTid, kLenB, kLenC, kW0, kLen, kOrgJ, kOrgK, kBk, kBj, kIEnd };  // kIEnd: affine kernel only
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
@@ -290,6 +304,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   constexpr int T = SM::T;
   [[maybe_unused]] constexpr int NN = SM::NN;
   constexpr int XW = SM::XW;
+  constexpr int LAG = SM::LAG, NB = SM::NB;
   constexpr int SH = TRACE ? 3 : 0;  // value scale 2^SH (tags in low bits)
   constexpr uint32_t NEG = (TRACE && LANES == 1) ? 0xF0000000u : Ops::kNeg;
   constexpr uint32_t kOneL = Ops::kOne;  // 1 per lane
@@ -308,7 +323,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   // Best (value, cell) of every open stream item, shared by the CTA's threads:
   // key = best_key(value, lin) (larger value, then smaller (i, j, k));
   // bcnt counts threads that finished the item (the last one flushes).
-  unsigned long long* const bkey = reinterpret_cast<unsigned long long*>(mbar + 2);     // [LANES][kSlots]
+  int32_t* const iend_s = reinterpret_cast<int32_t*>(mbar + 4);                          // [LANES] stream ends
+  unsigned long long* const bkey = reinterpret_cast<unsigned long long*>(mbar + 6);     // [LANES][kSlots]
   uint32_t* const bcnt = reinterpret_cast<uint32_t*>(bkey + LANES * SM::kSlots);         // [LANES][kSlots]
 
   constexpr int GN = G * N;
@@ -334,23 +350,32 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   const int k0 = cc * N;
   const int left = cc ? tile - 1 : T;
   const int up = r ? tile - G : T;
-  const int skew = r + cc;
+  const int skew = LAG * (r + cc);
   const int g2 = args.g2;
   const int ag2 = -g2;
   const uint32_t one = args.one;
   // TRACE: run-time powers of two and -1 keep the record packing on the FMA pipe
   [[maybe_unused]] const uint32_t mone = 0u - one;
   [[maybe_unused]] const uint32_t pw[5] = {one, one << 3, one << 6, one << 9, one << 12};
-  auto LS = [&](int l, int f) -> int32_t& { return lst[(l * SM::kLaneFields + f) * T + t]; };
+  // single-plane kernels: origin 0, one block (constants the compiler folds)
+  [[maybe_unused]] int32_t cst[LANES][4];
+#pragma unroll
+  for (int l = 0; l < LANES; ++l) cst[l][0] = cst[l][1] = 0, cst[l][2] = cst[l][3] = 1;
+  auto LS = [&](int l, int f) -> int32_t& {
+    if constexpr (!BLOCKS) {
+      if (f >= kOrgJ) return cst[l][f - kOrgJ];
+    }
+    return lst[(l * SM::kLaneFields + f) * T + t];
+  };
 
-  for (int w = t; w < 2 * XW; w += T) xbuf[((w / XW) * (T + 1) + T) * XW + w % XW] = NEG;
+  for (int w = t; w < NB * XW; w += T) xbuf[((w / XW) * (T + 1) + T) * XW + w % XW] = NEG;
   for (int w = t; w < LANES * SM::kSlots; w += T) {
     bkey[w] = 0ull;
     bcnt[w] = 0u;
   }
   if (t == 0) {
-    mbar_init(&mbar[0], T);
-    mbar_init(&mbar[1], T);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], T);
   }
 
   // hot per-lane state in registers
@@ -401,11 +426,13 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     if (rec.x < 0 && it < iend) len = rec.z;  // null item: the lane idles for len slices
     if (rec.x >= 0) {
       id = rec.x;
-      J = rec.y >> 16;
-      K = rec.y & 0xFFFF;
+      if constexpr (BLOCKS) {
+        J = rec.y >> 16;
+        K = rec.y & 0xFFFF;
+        Bj = rec.w >> 16;
+        Bk = rec.w & 0xFFFF;
+      }
       len = rec.z;
-      Bj = rec.w >> 16;
-      Bk = rec.w & 0xFFFF;
       const uint4 d0 = __ldg(reinterpret_cast<const uint4*>(args.desc + id));
       const uint4 d1 = __ldg(reinterpret_cast<const uint4*>(args.desc + id) + 1);
       a_ = static_cast<int>(d0.x);
@@ -547,7 +574,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     const int it = args.stream_off[sbase + l];
     const int ie = args.stream_off[sbase + l + 1];
     LS(l, kItem) = it;
-    LS(l, kIEnd) = ie;
+    if (t == 0) iend_s[l] = ie;
     si[l] = 0;
     s0word[l] = 0;
     first[l] = fetch(l, it, ie);
@@ -582,22 +609,36 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 
   __syncthreads();
 
-  // Mailbox protocol: step s publishes into xbuf[s & 1] and arrives on
-  // mbar[s & 1]; step s+1 waits for that phase before it reads.  A thread
-  // publishing at step s+1 has waited for every thread's step-s arrival,
-  // which follows that thread's step-s reads of the same buffer, so the
-  // double buffer is race-free without __syncthreads and the per-step tail
+  // Mailbox protocol: step s publishes into xbuf[s % NB] and arrives on
+  // mbar[s % NB]; step s + LAG waits for that phase before it reads.  LAG = 1:
+  // a thread publishing at step s+1 has waited for every thread's step-s
+  // arrival, which follows that thread's step-s reads of the same buffer.
+  // LAG = 2: a thread reads at step s what its neighbours published at step
+  // s - 2 (waits for phase s - 2), and before it overwrites buffer s % 3 -
+  // read by its neighbours at step s - 1 - it waits for phase s - 1.  Either
+  // way the ring is race-free without __syncthreads, and the per-step tail
   // work (extraction, lane switches, prefetch) overlaps the slowest warp.
-  const int nsteps = args.cta_steps[blockIdx.x];
+  // The host's step count covers a LAG = 1 pipeline; the extra fill is added here.
+  const int nsteps = args.cta_steps[blockIdx.x] + (LAG - 1) * 2 * (G - 1);
+  // phase of step q: the (q / NB)-th completion of mbar[q % NB]
+  auto wait_step = [&](int q) { mbar_wait(&mbar[q % NB], static_cast<uint32_t>(q / NB) & 1u); };
+  // LAG = 2: before a thread publishes (or arrives) at step s, the buffer
+  // readers of step s - 1 are done (this also orders its arrivals per mbarrier)
+  auto wait_free = [&](int s_) {
+    if constexpr (LAG > 1) {
+      if (s_ >= 1) wait_step(s_ - 1);
+    }
+  };
   for (int s = 0; s < nsteps; ++s) {
-    const int buf = s & 1;
+    const int buf = s % NB;
+    const int rbuf = (s + 1) % NB;  // == (s - LAG) mod NB
     bool any = false;
 #pragma unroll
     for (int l = 0; l < LANES; ++l) any |= !(flags[l] & kDone);
     const bool active = s >= skew && any;
     // Every thread (active or idle) waits for the previous phase before it
     // arrives again: no thread can arrive on mbar[b] twice within one phase.
-    if (s > 0) mbar_wait(&mbar[buf ^ 1], static_cast<uint32_t>((s - 1) >> 1) & 1u);
+    if (s >= LAG) wait_step(s - LAG);
     // A tile that holds no real cell of any live lane this step (padding
     // beyond b / c, or the padded slices of a block item) skips the sweep: its
     // values only ever feed other padding, and its warp's issue slots go to
@@ -617,8 +658,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       uint32_t Cu[N + 1][N + 1];
       // ---- 1. new halos (published by the neighbours at step s-1) --------
       {
-        const uint4* xu = reinterpret_cast<const uint4*>(xbuf + ((buf ^ 1) * (T + 1) + up) * XW);
-        const uint4* xl = reinterpret_cast<const uint4*>(xbuf + ((buf ^ 1) * (T + 1) + left) * XW + SM::DR);
+        const uint4* xu = reinterpret_cast<const uint4*>(xbuf + (rbuf * (T + 1) + up) * XW);
+        const uint4* xl = reinterpret_cast<const uint4*>(xbuf + (rbuf * (T + 1) + left) * XW + SM::DR);
 #pragma unroll
         for (int v = 0; v < SM::DR / 4; ++v) {
           const uint4 e = xu[v];
@@ -907,6 +948,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       sweep_tile();
 
       // ---- 5. publish right column / down row (+ corner) ----------------
+      wait_free(s);
       {
         uint4* xo = reinterpret_cast<uint4*>(xbuf + (buf * (T + 1) + tile) * XW);
 #pragma unroll
@@ -1175,6 +1217,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = Cu[P][Q];
 
      } else {
+      wait_free(s);
       mbar_arrive_group(&mbar[buf]);
      }
 
@@ -1222,8 +1265,8 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         const int it0 = LS(0, kItem) + 1, it1 = LS(LANES - 1, kItem) + 1;
         LS(0, kItem) = it0;
         LS(LANES - 1, kItem) = it1;
-        const LaneLoad l0 = fetch(0, it0, LS(0, kIEnd));
-        const LaneLoad l1 = fetch(LANES - 1, it1, LS(LANES - 1, kIEnd));
+        const LaneLoad l0 = fetch(0, it0, iend_s[0]);
+        const LaneLoad l1 = fetch(LANES - 1, it1, iend_s[LANES - 1]);
         if constexpr (LANES == 2) tables_both(l0, l1);
 #pragma unroll
         for (int l = 0; l < LANES; ++l) si[l] = 0;
@@ -1239,7 +1282,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           if (!sw[l]) continue;
           const int it = LS(l, kItem) + 1;
           LS(l, kItem) = it;
-          setup(l, it, LS(l, kIEnd));
+          setup(l, it, iend_s[l]);
           si[l] = 0;
           switched = true;
 #pragma unroll
@@ -1250,6 +1293,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         if (kPackFaces && switched) paired = lockstep();
       }
     } else {
+      wait_free(s);
       mbar_arrive_group(&mbar[buf]);
     }
     // next slice's s0 word (consumed after the barrier: latency hidden)
