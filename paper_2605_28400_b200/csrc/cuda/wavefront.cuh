@@ -19,7 +19,9 @@
 //    one VIADDMNMX.S16x2 / VIMNMX3.S16x2 advances two triplets.
 //  * Scores are computed in a gap-shifted space M' = M - g2*(i+j+k)
 //    (g2 = 2*gap), which zeroes the weight of the three single-residue
-//    terms: 6 instructions per cell (IADD3 + 4 VIADDMNMX + VIMNMX3).
+//    terms.  The tile is updated in place (no previous-slice copy); per cell
+//    2 VIADDMNMX + 2 VIMNMX3 + 2 packed adds (IMAD), sigma12' folded out of
+//    max(t1, t4).
 //  * Neighbour boundaries (right column / down row + corner) go through a
 //    double-buffered shared-memory mailbox, one __syncthreads per step.
 //  * Exactness: all arithmetic is integer; lane width is chosen by the host
@@ -51,8 +53,6 @@ constexpr uint32_t kTagT5 = 2, kTagT6 = 1, kTagT7 = 0, kTagStop = 7;
 // w holds the 3-bit codes of sweep-order cells 10w .. 10w+9: cell m < 5 at
 // bit 3m, cell m >= 5 at bit 16 + 3(m - 5) (two 15-bit halves).
 constexpr int kDirWords = 10;
-constexpr uint32_t kTraceC1 = 0xFFFFFFFAu;  // int32 lanes: -6
-constexpr uint32_t kTraceC2 = 0xFFF9FFFAu;  // s16x2 lanes: -6 per lane (the low lane always carries)
 // Sweep-order index of cell (p, q) of an n x n tile visited by anti-diagonals
 // (d = p + q, p ascending); with n = G it is the thread index of tile (r, c)
 // under the kernel's anti-diagonal thread map.
@@ -601,11 +601,13 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
   };
   bool paired = lockstep();
 
-  uint32_t Pv[N + 1][N + 1];
+  // the tile in registers (row / column 0: the halos), updated in place:
+  // slice i - 1 until the sweep of slice i overwrites it cell by cell
+  uint32_t Cu[N + 1][N + 1];
 #pragma unroll
   for (int P = 0; P <= N; ++P)
 #pragma unroll
-    for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = NEG;
+    for (int Q = 0; Q <= N; ++Q) Cu[P][Q] = NEG;
 
   __syncthreads();
 
@@ -655,8 +657,67 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     }
     if (active) {
      if (work) {
-      uint32_t Cu[N + 1][N + 1];
-      // ---- 1. new halos (published by the neighbours at step s-1) --------
+      // ---- 1. per-slice sigma row / column tables -----------------------
+      uint32_t sel = 0;  // LANES == 2: PRMT selector; LANES == 1: code
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        const int pos = si[l] - 1;
+        const uint32_t code = (pos >= 0 && (!BLOCKS || pos < la[l])) ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
+        if constexpr (LANES == 1) {
+          sel = code;
+        } else {
+          const uint32_t b = code + 4u * l;
+          sel |= (b | ((b | 8u) << 4)) << (8 * l);
+        }
+      }
+      auto sig_row = [&](const unsigned char* tab, int p) -> uint32_t {
+        if constexpr (LANES == 1) {
+          return static_cast<uint32_t>(static_cast<int>(
+              reinterpret_cast<const int16_t*>(tab)[(size_t(p) * T + t) * 4 + sel]));
+        } else {
+          const uint2 e = reinterpret_cast<const uint2*>(tab)[p * T + t];
+          return prmt(e.x, e.y, sel);
+        }
+      };
+      uint32_t s02[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        s02[q] = sig_row(tab2, q);
+        if constexpr (TRACE) s02[q] = s02[q] * 8u + kTagT3 * kOneL;
+      }
+      // TRACE: t1's column term sigma02' with tag 4 - 6 (lane-exact), so that
+      // t1 = W + a2c + sg carries tag 5 + 4 - 6 + 3 = 6
+      [[maybe_unused]] uint32_t a2c[TRACE ? N : 1];
+      if constexpr (TRACE) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) a2c[q] = Ops::addmax(s02[q], Ops::splat(-6), NEG);
+      }
+      uint32_t a1v[N];
+#pragma unroll
+      for (int p = 0; p < N; ++p) {
+        a1v[p] = sig_row(tab1, p);
+        if constexpr (TRACE) a1v[p] = a1v[p] * 8u + kTagT2 * kOneL;
+      }
+
+      // ---- 2. previous-slice terms of the halo, then the new halos -------
+      // The tile is updated in place: Cu[P][Q] holds M'(i - 1) until the
+      // sweep overwrites it with M'(i).  Two partial sums of a previous-slice
+      // value are formed before it is overwritten (packed adds on the FMA
+      // pipe, carry-free: values >= 0 or NEG-derived, weights >= 0):
+      //   W[P][Q] = M'(i-1, P-1, Q) + sigma01'(P)  (t2 of (P, Q); t1 of (P, Q+1))
+      //   Z[P][Q] = M'(i-1, P, Q-1) + sigma02'(Q)  (t3 of (P, Q))
+      // so the recurrence needs 2 DPX + 2 three-way max per cell and no
+      // previous-slice copy.  The halo row / column feed W[1][*], W[*][0] and
+      // Z[*][1] before this slice's halos replace them.
+      uint32_t W[N + 1][N + 1], Z[N + 1][N + 1];
+#pragma unroll
+      for (int Q = 0; Q <= N; ++Q) W[1][Q] = fma_add(Cu[0][Q], one, a1v[0]);
+#pragma unroll
+      for (int P = 2; P <= N; ++P) W[P][0] = fma_add(Cu[P - 1][0], one, a1v[P - 1]);
+#pragma unroll
+      for (int P = 1; P <= N; ++P) Z[P][1] = fma_add(Cu[P][0], one, s02[0]);
+
+      // new halos (published by the neighbours LAG steps earlier)
       {
         const uint4* xu = reinterpret_cast<const uint4*>(xbuf + (rbuf * (T + 1) + up) * XW);
         const uint4* xl = reinterpret_cast<const uint4*>(xbuf + (rbuf * (T + 1) + left) * XW + SM::DR);
@@ -751,45 +812,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
       }
 
-      // ---- 2. per-slice sigma row / column tables -----------------------
-      uint32_t sel = 0;  // LANES == 2: PRMT selector; LANES == 1: code
-#pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        const int pos = si[l] - 1;
-        const uint32_t code = (pos >= 0 && (!BLOCKS || pos < la[l])) ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
-        if constexpr (LANES == 1) {
-          sel = code;
-        } else {
-          const uint32_t b = code + 4u * l;
-          sel |= (b | ((b | 8u) << 4)) << (8 * l);
-        }
-      }
-      auto sig_row = [&](const unsigned char* tab, int p) -> uint32_t {
-        if constexpr (LANES == 1) {
-          return static_cast<uint32_t>(static_cast<int>(
-              reinterpret_cast<const int16_t*>(tab)[(size_t(p) * T + t) * 4 + sel]));
-        } else {
-          const uint2 e = reinterpret_cast<const uint2*>(tab)[p * T + t];
-          return prmt(e.x, e.y, sel);
-        }
-      };
-      uint32_t s02[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        s02[q] = sig_row(tab2, q);
-        if constexpr (TRACE) s02[q] = s02[q] * 8u + kTagT3 * kOneL;
-      }
-      // t1's column term: sigma02' with tag 4 - 6, so that t1 = Pv + a1 + a2c + sg
-      // carries tag 5 + 4 - 6 + 3 = 6 (added on the FMA pipe: the -6 per lane
-      // is exact because every low-lane sum it meets is >= 9 or NEG-derived)
-      [[maybe_unused]] uint32_t a2c[TRACE ? N : 1];
-#ifndef TA_TRACE_Y3
-      if constexpr (TRACE) {
-#pragma unroll
-        for (int q = 0; q < N; ++q) a2c[q] = s02[q] + (LANES == 2 ? kTraceC2 : kTraceC1);
-      }
-#endif
-
       // ---- 3. forced cells (reference initialisation, oracle.cpp:30-39) --
       // global: M(0,0,0) = 0; semi: axis cells are 0 in M-space.
       uint32_t fcorner = NEG;
@@ -834,7 +856,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
       }
 
-      // ---- 4. the tile: 6 integer instructions per cell -----------------
+      // ---- 4. the tile: 2 DPX + 2 three-way max + 2 packed adds per cell --
       // TRACE: direction records of this step, one pointer per live lane
       [[maybe_unused]] uint32_t* dptr[LANES];
       [[maybe_unused]] bool dok[LANES];
@@ -860,12 +882,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       // independent, so the row / column dependencies of the recurrence are
       // ~N instructions apart instead of back to back.  sigma12' is stored in
       // the same order (4 cells per LDS.128).
-      uint32_t a1v[N];
-#pragma unroll
-      for (int p = 0; p < N; ++p) {
-        a1v[p] = sig_row(tab1, p);
-        if constexpr (TRACE) a1v[p] = a1v[p] * 8u + kTagT2 * kOneL;
-      }
       uint4 sg4 = make_uint4(0, 0, 0, 0);
       [[maybe_unused]] uint32_t fd = flrow;  // local floor of diagonal d (depends on P + Q only)
       [[maybe_unused]] uint32_t frv = frb, fcv = fcb;  // semi: start of the next row-1 / column-1 cell
@@ -884,30 +900,19 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const uint32_t sg = (k & 3) == 0 ? sg4.x : (k & 3) == 1 ? sg4.y : (k & 3) == 2 ? sg4.z : sg4.w;
           [[maybe_unused]] const int ks = k;  // sweep-order index of this cell
           ++k;
-          const uint32_t a1 = a1v[P - 1];
-          const uint32_t a2 = s02[Q - 1];
           uint32_t x;
           if constexpr (!TRACE) {
-            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2);  // t1 partial (FMA pipe)
-            x = Ops::addmax(Pv[P - 1][Q], a1, Pv[P][Q]);             // max(t2, t5)
-            x = Ops::addmax(Pv[P][Q - 1], a2, x);                    // t3
-            x = Ops::addmax(y, sg, x);                               // t1
-            x = Ops::addmax(Cu[P - 1][Q - 1], sg, x);                // t4
-            x = Ops::max3(x, Cu[P - 1][Q], Cu[P][Q - 1]);            // t6, t7
+            const uint32_t c = Ops::addmax(W[P][Q - 1], s02[Q - 1], Cu[P - 1][Q - 1]);  // max(t1, t4) - sg
+            x = Ops::addmax(c, sg, Z[P][Q]);                                           // t1, t4 vs t3
+            x = Ops::max3(x, W[P][Q], Cu[P][Q]);                                       // t2, t5 (Cu[P][Q]: slice i-1)
+            x = Ops::max3(x, Cu[P - 1][Q], Cu[P][Q - 1]);                              // t6, t7
           } else {
-            // tags: a1, a2, sg carry 5, 4, 3; t1 = 5 + (4 - 6) + 3 = 6
-#ifdef TA_TRACE_Y3
-            const uint32_t y = fma_add(fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2), one,
-                                       LANES == 2 ? kTraceC2 : kTraceC1);
-#else
-            const uint32_t y = fma_add(fma_add(Pv[P - 1][Q - 1], one, a1), one, a2c[Q - 1]);
-#endif
-            x = Ops::addmax(Pv[P - 1][Q], a1, Cu[P][Q - 1]);         // max(t2, t7)
-            x = Ops::addmax(Pv[P][Q - 1], a2, x);                    // t3
-            x = Ops::addmax(y, sg, x);                               // t1
-            x = Ops::addmax(Cu[P - 1][Q - 1], sg, x);                // t4
-            x = Ops::addmax(Pv[P][Q], kTagT5 * kOneL, x);            // t5
-            x = Ops::addmax(Cu[P - 1][Q], kTagT6 * kOneL, x);        // t6
+            // tags: W, Z, sg carry 5, 4, 3; t1 = 5 + (4 - 6) + 3 = 6; t5, t6, t7: 2, 1, 0
+            const uint32_t c = Ops::addmax(W[P][Q - 1], a2c[Q - 1], Cu[P - 1][Q - 1]);  // tags 3 / 0
+            x = Ops::addmax(c, sg, Z[P][Q]);                                            // t1 6, t4 3, t3 4
+            x = Ops::max3(x, W[P][Q], Cu[P][Q - 1]);                                    // t2 5, t7 0
+            x = Ops::addmax(Cu[P][Q], kTagT5 * kOneL, x);                               // t5
+            x = Ops::addmax(Cu[P - 1][Q], kTagT6 * kOneL, x);                           // t6
           }
           if constexpr (MODE == kLocal) x = Ops::addmax(fd, one ^ 1u, x);  // floor 0 (oracle.cpp:59), fused form
           if constexpr (MODE == kGlobal || MODE == kSemi) {
@@ -941,6 +946,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               }
             }
           }
+          // the previous-slice value of this cell feeds (P + 1, Q) and (P, Q + 1)
+          if (P < N) W[P + 1][Q] = fma_add(Cu[P][Q], one, a1v[P]);
+          if (Q < N) Z[P][Q + 1] = fma_add(Cu[P][Q], one, s02[Q]);
           Cu[P][Q] = x;
         }
       }
@@ -1210,12 +1218,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
       }
 
-      // ---- 8. previous slice := this slice ------------------------------
-#pragma unroll
-      for (int P = 0; P <= N; ++P)
-#pragma unroll
-        for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = Cu[P][Q];
-
      } else {
       wait_free(s);
       mbar_arrive_group(&mbar[buf]);
@@ -1273,7 +1275,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
         for (int P = 0; P <= N; ++P)
 #pragma unroll
-          for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = NEG;
+          for (int Q = 0; Q <= N; ++Q) Cu[P][Q] = NEG;
         if constexpr (kPackFaces) paired = lockstep();
       } else {
         [[maybe_unused]] bool switched = false;
@@ -1288,7 +1290,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
 #pragma unroll
           for (int P = 0; P <= N; ++P)
 #pragma unroll
-            for (int Q = 0; Q <= N; ++Q) Pv[P][Q] = lop_sel(Pv[P][Q], NEG, Ops::mask(l));
+            for (int Q = 0; Q <= N; ++Q) Cu[P][Q] = lop_sel(Cu[P][Q], NEG, Ops::mask(l));
         }
         if (kPackFaces && switched) paired = lockstep();
       }
