@@ -900,18 +900,24 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const uint32_t sg = (k & 3) == 0 ? sg4.x : (k & 3) == 1 ? sg4.y : (k & 3) == 2 ? sg4.z : sg4.w;
           [[maybe_unused]] const int ks = k;  // sweep-order index of this cell
           ++k;
+          // the previous-slice value of this cell feeds (P + 1, Q) and (P, Q + 1);
+          // its last use is the cell's own final max (t5), so the new value can
+          // take its register (no permutation moves at the loop back edge)
+          const uint32_t old = Cu[P][Q];
+          if (P < N) W[P + 1][Q] = fma_add(old, one, a1v[P]);
+          if (Q < N) Z[P][Q + 1] = fma_add(old, one, s02[Q]);
           uint32_t x;
           if constexpr (!TRACE) {
             const uint32_t c = Ops::addmax(W[P][Q - 1], s02[Q - 1], Cu[P - 1][Q - 1]);  // max(t1, t4) - sg
             x = Ops::addmax(c, sg, Z[P][Q]);                                           // t1, t4 vs t3
-            x = Ops::max3(x, W[P][Q], Cu[P][Q]);                                       // t2, t5 (Cu[P][Q]: slice i-1)
+            x = Ops::max3(x, W[P][Q], old);                                            // t2, t5
             x = Ops::max3(x, Cu[P - 1][Q], Cu[P][Q - 1]);                              // t6, t7
           } else {
             // tags: W, Z, sg carry 5, 4, 3; t1 = 5 + (4 - 6) + 3 = 6; t5, t6, t7: 2, 1, 0
             const uint32_t c = Ops::addmax(W[P][Q - 1], a2c[Q - 1], Cu[P - 1][Q - 1]);  // tags 3 / 0
             x = Ops::addmax(c, sg, Z[P][Q]);                                            // t1 6, t4 3, t3 4
             x = Ops::max3(x, W[P][Q], Cu[P][Q - 1]);                                    // t2 5, t7 0
-            x = Ops::addmax(Cu[P][Q], kTagT5 * kOneL, x);                               // t5
+            x = Ops::addmax(old, kTagT5 * kOneL, x);                                    // t5
             x = Ops::addmax(Cu[P - 1][Q], kTagT6 * kOneL, x);                           // t6
           }
           if constexpr (MODE == kLocal) x = Ops::addmax(fd, one ^ 1u, x);  // floor 0 (oracle.cpp:59), fused form
@@ -946,9 +952,6 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
               }
             }
           }
-          // the previous-slice value of this cell feeds (P + 1, Q) and (P, Q + 1)
-          if (P < N) W[P + 1][Q] = fma_add(Cu[P][Q], one, a1v[P]);
-          if (Q < N) Z[P][Q + 1] = fma_add(Cu[P][Q], one, s02[Q]);
           Cu[P][Q] = x;
         }
       }
