@@ -308,12 +308,14 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
   };
   bool paired = lockstep();
 
-  // previous-slice state (incl. the halo row / column received last step)
-  uint32_t pB[N + 1][N + 1], pE2[N + 1][N + 1], pE3[N + 1][N + 1], pE5[N + 1][N + 1];
+  // B, E2, E3, E5 of the tile (incl. the halo row / column), updated in
+  // place: slice i - 1 until the sweep of slice i overwrites a cell (the
+  // slice i-1 terms a later cell needs are formed first, see the sweep)
+  uint32_t cB[N + 1][N + 1], cE2[N + 1][N + 1], cE3[N + 1][N + 1], cE5[N + 1][N + 1];
 #pragma unroll
   for (int P = 0; P <= N; ++P)
 #pragma unroll
-    for (int Q = 0; Q <= N; ++Q) pB[P][Q] = pE2[P][Q] = pE3[P][Q] = pE5[P][Q] = NEG;
+    for (int Q = 0; Q <= N; ++Q) cB[P][Q] = cE2[P][Q] = cE3[P][Q] = cE5[P][Q] = NEG;
 
   __syncthreads();
 
@@ -326,9 +328,51 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
     const bool active = s >= skew && any;
     if (s > 0) mbar_wait(&mbar[buf ^ 1], static_cast<uint32_t>((s - 1) >> 1) & 1u);
     if (active) {
-      uint32_t cB[N + 1][N + 1], cE2[N + 1][N + 1], cE3[N + 1][N + 1], cE4[N + 1][N + 1], cE5[N + 1][N + 1],
-          cE6[N + 1][N + 1], cE7[N + 1][N + 1];
+      uint32_t cE4[N + 1][N + 1], cE6[N + 1][N + 1], cE7[N + 1][N + 1];
       uint32_t rec[TRACE ? NN : 1];
+      // ---- 2. sigma' of this slice's s0 residue against the tile's s1 / s2
+      uint32_t sel = 0;
+#pragma unroll
+      for (int l = 0; l < LANES; ++l) {
+        const int pos = si[l] - 1;
+        const uint32_t code = (pos >= 0 && (!BLOCKS || pos < la[l])) ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
+        if constexpr (LANES == 1) {
+          sel = code;
+        } else {
+          const uint32_t b = code + 4u * l;
+          sel |= (b | ((b | 8u) << 4)) << (8 * l);
+        }
+      }
+      auto sig_row = [&](const unsigned char* tab, int p) -> uint32_t {
+        if constexpr (LANES == 1) {
+          return static_cast<uint32_t>(
+              static_cast<int>(reinterpret_cast<const int16_t*>(tab)[(size_t(p) * T + t) * 4 + sel]) * SC);
+        } else {
+          const uint2 e = reinterpret_cast<const uint2*>(tab)[p * T + t];
+          return prmt(e.x, e.y, sel);
+        }
+      };
+      uint32_t s02[N], a1v[N];
+#pragma unroll
+      for (int q = 0; q < N; ++q) s02[q] = sig_row(tab2, q);
+#pragma unroll
+      for (int p = 0; p < N; ++p) a1v[p] = sig_row(tab1, p);
+      // slice i-1 partial sums of the halo (before this slice's halos replace
+      // it): Y[P][Q] = B'(P-1, Q-1) + s01' + s02' (V1), V2[P][Q] = E2'(P-1, Q)
+      // + s01', V3[P][Q] = E3'(P, Q-1) + s02'; the sweep forms the interior ones
+      uint32_t Y[N + 1][N + 1], V2[N + 1][N + 1], V3[N + 1][N + 1];
+#pragma unroll
+      for (int Q = 1; Q <= N; ++Q) {
+        Y[1][Q] = fma_add(fma_add(cB[0][Q - 1], one, a1v[0]), one, s02[Q - 1]);
+        V2[1][Q] = fma_add(cE2[0][Q], one, a1v[0]);
+      }
+#pragma unroll
+      for (int P = 1; P <= N; ++P) {
+        if (P > 1) Y[P][1] = fma_add(fma_add(cB[P - 1][0], one, a1v[P - 1]), one, s02[0]);
+        V3[P][1] = fma_add(cE3[P][0], one, s02[0]);
+      }
+
+
       // ---- 1. halos of this slice (published by the neighbours at step s-1)
       const uint4* xin = reinterpret_cast<const uint4*>(xbuf + (buf ^ 1) * XW * (T + 1));
 #pragma unroll
@@ -460,32 +504,6 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         }
       }
 
-      // ---- 2. sigma' of this slice's s0 residue against the tile's s1 / s2
-      uint32_t sel = 0;
-#pragma unroll
-      for (int l = 0; l < LANES; ++l) {
-        const int pos = si[l] - 1;
-        const uint32_t code = (pos >= 0 && (!BLOCKS || pos < la[l])) ? (s0word[l] >> ((pos & 15) * 2)) & 3u : 0u;
-        if constexpr (LANES == 1) {
-          sel = code;
-        } else {
-          const uint32_t b = code + 4u * l;
-          sel |= (b | ((b | 8u) << 4)) << (8 * l);
-        }
-      }
-      auto sig_row = [&](const unsigned char* tab, int p) -> uint32_t {
-        if constexpr (LANES == 1) {
-          return static_cast<uint32_t>(
-              static_cast<int>(reinterpret_cast<const int16_t*>(tab)[(size_t(p) * T + t) * 4 + sel]) * SC);
-        } else {
-          const uint2 e = reinterpret_cast<const uint2*>(tab)[p * T + t];
-          return prmt(e.x, e.y, sel);
-        }
-      };
-      uint32_t s02[N];
-#pragma unroll
-      for (int q = 0; q < N; ++q) s02[q] = sig_row(tab2, q);
-
       // ---- 3. starts (SPEC-AFFINE.md): global origin, semi axis cells, local every cell
       // biased, gap-shifted value of M = 0 at (i, j, k): bias + |g2| (i + j + k)
       uint32_t stbase = NEG;  // local: start value of the tile's cell (1, 1)
@@ -536,7 +554,6 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         [[maybe_unused]] uint32_t frv = frb, fcv = fcb;
 #pragma unroll
         for (int P = 1; P <= N; ++P) {
-          const uint32_t a1 = sig_row(tab1, P - 1);
           [[maybe_unused]] uint32_t st = strow;
           if constexpr (MODE == kLocal) {
             if (P < N) strow = fma_add(strow, one, ag2s);
@@ -545,7 +562,6 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           for (int Q = 1; Q <= N; ++Q) {
             const int cell = (P - 1) * N + (Q - 1);
             const uint32_t sg = s12w[cell * T + t];
-            const uint32_t a2 = s02[Q - 1];
             // start value of this cell (NEG where no alignment may start)
             uint32_t start = NEG;
             if constexpr (MODE == kLocal) {
@@ -564,12 +580,17 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
                 }
               }
             }
-            const uint32_t y = fma_add(fma_add(pB[P - 1][Q - 1], one, a1), one, a2);
-            uint32_t v1 = Ops::addmax(y, sg, start);
-            uint32_t v2 = fma_add(pE2[P - 1][Q], one, a1);
-            uint32_t v3 = fma_add(pE3[P][Q - 1], one, a2);
+            // slice i-1 values of this cell: form the partial sums the later
+            // cells need, so the cell can be overwritten in place
+            const uint32_t oB = cB[P][Q], oE2 = cE2[P][Q], oE3 = cE3[P][Q];
+            if (P < N && Q < N) Y[P + 1][Q + 1] = fma_add(fma_add(oB, one, a1v[P]), one, s02[Q]);
+            if (P < N) V2[P + 1][Q] = fma_add(oE2, one, a1v[P]);
+            if (Q < N) V3[P][Q + 1] = fma_add(oE3, one, s02[Q]);
+            uint32_t v1 = Ops::addmax(Y[P][Q], sg, start);
+            uint32_t v2 = V2[P][Q];
+            uint32_t v3 = V3[P][Q];
             uint32_t v4 = fma_add(cE4[P - 1][Q - 1], one, sg);
-            uint32_t v5 = pE5[P][Q];
+            uint32_t v5 = cE5[P][Q];
             uint32_t v6 = cE6[P - 1][Q];
             uint32_t v7 = cE7[P][Q - 1];
             [[maybe_unused]] uint32_t rc = 0;
@@ -847,17 +868,6 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         }
       }
 
-      // ---- 8. this slice becomes the previous one (halos included) ------------
-#pragma unroll
-      for (int P = 0; P <= N; ++P)
-#pragma unroll
-        for (int Q = 0; Q <= N; ++Q) {
-          pB[P][Q] = cB[P][Q];
-          pE2[P][Q] = cE2[P][Q];
-          pE3[P][Q] = cE3[P][Q];
-          pE5[P][Q] = cE5[P][Q];
-        }
-
       // ---- 9. advance the lanes ---------------------------------------------------
       [[maybe_unused]] bool switched = false;
 #pragma unroll
@@ -885,10 +895,10 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
         for (int P = 0; P <= N; ++P)
 #pragma unroll
           for (int Q = 0; Q <= N; ++Q) {
-            pB[P][Q] = lop_sel(pB[P][Q], NEG, Ops::mask(l));
-            pE2[P][Q] = lop_sel(pE2[P][Q], NEG, Ops::mask(l));
-            pE3[P][Q] = lop_sel(pE3[P][Q], NEG, Ops::mask(l));
-            pE5[P][Q] = lop_sel(pE5[P][Q], NEG, Ops::mask(l));
+            cB[P][Q] = lop_sel(cB[P][Q], NEG, Ops::mask(l));
+            cE2[P][Q] = lop_sel(cE2[P][Q], NEG, Ops::mask(l));
+            cE3[P][Q] = lop_sel(cE3[P][Q], NEG, Ops::mask(l));
+            cE5[P][Q] = lop_sel(cE5[P][Q], NEG, Ops::mask(l));
           }
       }
       if (kPackFaces && switched) paired = lockstep();
