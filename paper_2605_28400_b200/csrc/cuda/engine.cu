@@ -560,6 +560,12 @@ struct ta_batch {
   DevBuf<int32_t> s_len, s_bad;
   DevBuf<uint32_t> s_dst;
   std::string plan_key;
+  // front cache of the linear score path: per-triplet validation, buckets and
+  // the plan key of the last run, reused while scheme and options are
+  // unchanged (the batch is immutable), so a repeated run does no O(n) host work
+  std::string front_key;
+  std::vector<int32_t> front_status, front_all_ok;
+  int64_t front_cells = 0;
   int last_mode = -1;
   bool last_rows = false;
   ~ta_batch() {
@@ -1297,8 +1303,22 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   const std::string cfg_msg = cfg_rc ? g_err : std::string();
   std::vector<std::vector<int32_t>> buckets(ta::kNumGrid);
   std::vector<int32_t> all_ok;
-  all_ok.reserve(size_t(n));
   int64_t max_bound_bucket[ta::kNumGrid] = {0};
+  const bool front_ok = !rows && !cfg_rc && scheme.gap_open == 0 && opt.gap_model != 1;
+  std::string fkey;
+  if (front_ok) {
+    fkey = std::to_string(scheme.match) + "," + std::to_string(scheme.mismatch) + "," + std::to_string(scheme.gap) +
+           "|" + std::to_string(opt.mode) + "," + std::to_string(opt.tile_size) + "," +
+           std::to_string(opt.team_width) + "," + std::to_string(opt.team_threads) + "," +
+           std::to_string(opt.lane_mode) + "," + std::to_string(opt.cell_budget);
+  }
+  const bool front_hit = front_ok && fkey == bt->front_key && !bt->plan_key.empty();
+  if (!front_hit) bt->front_key.clear();
+  if (front_hit) {
+    bt->status = bt->front_status;
+    all_ok = bt->front_all_ok;
+  } else {
+  all_ok.reserve(size_t(n));
   for (int64_t t = 0; t < n; ++t) {
     if (bt->status[size_t(t)] != TA_OK) continue;
     const int32_t A = bt->a[size_t(t)], B = bt->b[size_t(t)], C = bt->c[size_t(t)];
@@ -1335,6 +1355,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     max_bound_bucket[gi] = std::max(max_bound_bucket[gi], lane_bound(scheme, A, B, C, g));
     all_ok.push_back(int32_t(t));
   }
+  }
   if (cfg_rc) g_err = cfg_msg;
   if (scheme.gap_open != 0 || opt.gap_model == 1) return run_affine(bt, scheme, opt, st, all_ok, rows);
 
@@ -1361,6 +1382,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     // plan key: mode + per-bucket (grid, lanes, ids) fingerprint
     std::string key = std::to_string(opt.mode);
     std::vector<int> lanes_of(ta::kNumGrid, 1);
+    if (!front_hit) {
     // largest grid: wave triplets, 128-wide-block triplets (prefer_t8), the rest
     const int gl = ta::kNumGrid - 1;
     std::vector<int32_t> wave_ids, rest_ids, t8_ids;
@@ -1403,6 +1425,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       }
       bt->plan_key = key;
     }
+    }  // !front_hit
     for (auto& bl : bt->plan_cache) {
       lanes_used = std::max(lanes_used, bl->lanes);
       ++nbuckets;
@@ -1585,7 +1608,17 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   }
   (void)rows_out;
   int64_t cells = 0;
-  for (int32_t id : all_ok) cells += int64_t(bt->a[size_t(id)]) * bt->b[size_t(id)] * bt->c[size_t(id)];
+  if (front_hit) {
+    cells = bt->front_cells;
+  } else {
+    for (int32_t id : all_ok) cells += int64_t(bt->a[size_t(id)]) * bt->b[size_t(id)] * bt->c[size_t(id)];
+    if (front_ok) {
+      bt->front_key = fkey;
+      bt->front_status = bt->status;
+      bt->front_all_ok = all_ok;
+      bt->front_cells = cells;
+    }
+  }
   bt->stats.kernel_ms = ms_total;
   bt->stats.wavefront_ms = ms_total - bt->stats.walker_ms;
   bt->stats.cells = cells;
@@ -1909,6 +1942,7 @@ static int batch_init(ta_batch* bt, DeviceCtx* ctx, int device, const char* seqs
   bt->plan_cache.clear();
   bt->aff_cache.clear();
   bt->plan_key.clear();
+  bt->front_key.clear();
   bt->stats = ta_stats{};
   bt->device = device;
   bt->ctx = ctx;

@@ -246,3 +246,26 @@ def test_many_long_triplets_mixed_block_widths(gpu_engine, oracle, mode):
             want = oracle.align(t, sch, mode)
             assert int(sc["status"][x]) == 0
             assert int(sc["score"][x]) == want["score"] and list(sc["end"][x]) == want["end"], (sch, mode, x)
+
+
+def test_device_batch_rerun_cache(gpu_engine):
+    """A resident batch re-run with the same scheme/options reuses its host
+    plan (front cache); any change of scheme, mode, options or an affine /
+    rows run in between must re-plan.  Every run equals a fresh one-shot run."""
+    seqs, offs = ta.generate("uniform:40:170:600", 0.05, 0.01, 21)
+    b = ta.DeviceBatch(seqs, offs)
+    seq = [((1, -1, -2, 0), 0), ((1, -1, -2, 0), 0), ((1, -1, -2, 0), 1), ((2, -1, -1, 0), 1),
+           ((1, -1, -2, -3), 0), ((1, -1, -2, 0), 1), ((1, -1, -2, 0), 2), ((1, -1, -2, 0), 2),
+           ((1, -1, -2, 0), 0)]
+    for sch, mode in seq:
+        b.run(ta.ScoringScheme(*sch), ta.AlignmentMode(mode), ta.EngineConfig(cell_budget=1 << 40))
+        got = b.fetch()
+        want = ta.align_arrays(seqs, offs, ta.ScoringScheme(*sch), ta.AlignmentMode(mode), cell_budget=1 << 40)
+        assert (got["status"] == want["status"]).all(), (sch, mode)
+        assert (got["score"] == want["score"]).all(), (sch, mode)
+        assert (got["end"] == want["end"]).all(), (sch, mode)
+    # an option change that fails every triplet, then the valid options again
+    b.run(ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(0), ta.EngineConfig(cell_budget=1))
+    assert (b.fetch()["status"] != 0).all()
+    b.run(ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(0), ta.EngineConfig(cell_budget=1 << 40))
+    assert (b.fetch()["status"] == 0).all()
