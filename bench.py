@@ -563,7 +563,7 @@ def main(argv=None):
     launch_s = statistics.median(wave_ms) / 1e3
     achieved = cells * OPS_PER_CELL / launch_s / 1e12 if launch_s > 0 else 0.0
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02b_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
