@@ -979,10 +979,23 @@ BucketLaunch* rows_plan(ta_batch* bt, size_t* used) {
 
 int launch_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
                   bool trace, const ta::WaveArgs& base, cudaStream_t st, int64_t* launches, size_t* used) {
-  BucketLaunch* bl = rows_plan(bt, used);
-  if (int rc = prepare_bucket(bt, ids, grid, lanes, mode, trace, st, bl)) return rc;
-  if (int rc = launch_prepared(bl, base, st, launches)) return rc;
-  bt->stats.padded_cells += bl->padded;
+  // few long triplets of the largest grid run in wave mode (their blocks
+  // spread over all CTAs, direction records in the same layout), the rest
+  // as sequential block items of one stream
+  std::vector<int32_t> wave, rest;
+  if (grid == ta::kGridSizes[ta::kNumGrid - 1]) {
+    split_wave(ids, bt->a, bt->b, bt->c, grid, bt->ctx->sms * lanes, &wave, &rest);
+  } else {
+    rest = ids;
+  }
+  for (int w = 0; w < 2; ++w) {
+    const std::vector<int32_t>& part = w ? wave : rest;
+    if (part.empty()) continue;
+    BucketLaunch* bl = rows_plan(bt, used);
+    if (int rc = prepare_bucket(bt, part, grid, lanes, mode, trace, st, bl, w == 1)) return rc;
+    if (int rc = launch_prepared(bl, base, st, launches)) return rc;
+    bt->stats.padded_cells += bl->padded;
+  }
   return TA_OK;
 }
 

@@ -26,18 +26,20 @@ struct KernelEntry {
 
 // lanes in {1, 2}; mode in {kGlobal, kSemi, kLocal}; trace with either lane width;
 // blk: 0 single-plane, 1 sequential multi-block items, 2 wave (multi-CTA)
-// blocks; blk > 0 exists for the largest grid only, blk == 2 without trace.
+// blocks; blk > 0 exists for the largest grid only.
 KernelEntry kernel_g4(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g8(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g12(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g16(int lanes, int mode, bool trace, int blk);
 KernelEntry kernel_g16_wave(int lanes, int mode);
+// wave mode with direction records (traceback of a few long triplets)
+KernelEntry kernel_g16_wave_trace(int lanes, int mode);
 // 16 x 16 grid of 8 x 8 tiles, multi-block items only (blk 1, no trace): long
 // triplets whose extents pad less in 128-wide blocks than in 160-wide ones
 KernelEntry kernel_g16_t8(int lanes, int mode);
 
 inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int blk) {
-  if (blk == 2) return (grid == 16 && !trace) ? kernel_g16_wave(lanes, mode) : KernelEntry{};
+  if (blk == 2) return grid != 16 ? KernelEntry{} : trace ? kernel_g16_wave_trace(lanes, mode) : kernel_g16_wave(lanes, mode);
   switch (grid) {
     case 4: return kernel_g4(lanes, mode, trace, blk);
     case 8: return kernel_g8(lanes, mode, trace, blk);
@@ -118,20 +120,20 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
   }                                                                                                \
   }
 
-#define TA_DEFINE_WAVE_TABLE(G)                                                        \
+#define TA_DEFINE_WAVE_TABLE(G, NAME, TR)                                              \
   namespace ta {                                                                       \
-  KernelEntry kernel_g##G##_wave(int lanes, int mode) {                                \
+  KernelEntry NAME(int lanes, int mode) {                                              \
     if (lanes == 1) {                                                                  \
       switch (mode) {                                                                  \
-        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, false, 2);                 \
-        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, false, 2);                     \
-        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, false, 2);                   \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 1, kGlobal, TR, 2);                    \
+        case kSemi: return TA_KERNEL_ENTRY(G, 1, kSemi, TR, 2);                        \
+        case kLocal: return TA_KERNEL_ENTRY(G, 1, kLocal, TR, 2);                      \
       }                                                                                \
     } else {                                                                           \
       switch (mode) {                                                                  \
-        case kGlobal: return TA_KERNEL_ENTRY(G, 2, kGlobal, false, 2);                 \
-        case kSemi: return TA_KERNEL_ENTRY(G, 2, kSemi, false, 2);                     \
-        case kLocal: return TA_KERNEL_ENTRY(G, 2, kLocal, false, 2);                   \
+        case kGlobal: return TA_KERNEL_ENTRY(G, 2, kGlobal, TR, 2);                    \
+        case kSemi: return TA_KERNEL_ENTRY(G, 2, kSemi, TR, 2);                        \
+        case kLocal: return TA_KERNEL_ENTRY(G, 2, kLocal, TR, 2);                      \
       }                                                                                \
     }                                                                                  \
     return {};                                                                         \
