@@ -44,7 +44,8 @@ struct AffArgs {
   uint32_t* __restrict__ dirs;              // TRACE: per-cell records
   union {
     const int64_t* __restrict__ dir_off;    // TRACE: per triplet, in uint4
-    uint64_t epoch;                         // wave mode (never TRACE): launch epoch, the high half of the tags
+    uint64_t epoch;                         // wave mode, score kernels: launch epoch, the high half of the tags
+                                            // (TRACE wave launches run once per freshly zeroed plan: epoch 1)
   };
   int32_t match_p, mismatch_p, g2;          // sigma' (= sigma - 2 gap) and 2 gap
   int32_t open;                             // gap_open (<= 0)
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               const bool real = LS(l, kTid) >= 0 && LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 &&
                                 LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
               if (!ok || !real) continue;
-              const uint32_t want = (static_cast<uint32_t>(args.epoch) << 16) + static_cast<uint32_t>(si[l]) + 1u;
+              const uint32_t want = ((TRACE ? 1u : static_cast<uint32_t>(args.epoch)) << 16) + static_cast<uint32_t>(si[l]) + 1u;
               const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.face_off[LS(l, kTid)];
               const int a1 = la[l] + 1;
               const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
@@ -639,7 +640,7 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
           if (!dn && !rt) continue;
           const int a1 = la[l] + 1;
           if constexpr (WAVE) {
-            const uint32_t tag = (static_cast<uint32_t>(args.epoch) << 16) + static_cast<uint32_t>(si[l]) + 1u;
+            const uint32_t tag = ((TRACE ? 1u : static_cast<uint32_t>(args.epoch)) << 16) + static_cast<uint32_t>(si[l]) + 1u;
             uint2* fb = reinterpret_cast<uint2*>(reinterpret_cast<uint64_t*>(args.faces) + args.face_off[LS(l, kTid)]);
             const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
             auto put = [&](uint2* d, int e, uint32_t v) { st_face(d + e, static_cast<uint32_t>(Ops::lane(v, l)), tag); };

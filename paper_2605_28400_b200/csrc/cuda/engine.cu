@@ -1107,7 +1107,13 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
       bl->epoch = 1;
     }
     args.face_off = bl->wave_base.ptr;  // wave: ring base per triplet (AffArgs)
-    args.epoch = bl->epoch;
+    if (args.dirs) {
+      // TRACE (dir_off shares the epoch's slot): the kernel tags with epoch 1,
+      // so a traceback plan is launched once, on rings zeroed by aff_prepare
+      if (bl->epoch != 1) return fail(TA_ERR_LOGIC, "affine traceback wave plan launched twice");
+    } else {
+      args.epoch = bl->epoch;
+    }
     for (const WaveRound& rd : bl->rounds) {
       ta::AffArgs ra = args;
       ra.stream_off = bl->soff.ptr + rd.soff_at;
@@ -1137,7 +1143,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
   }
   const int lanes = (!rows && aff_s16_ok(scheme, maxb)) ? 2 : 1;
   // few long triplets: spread their blocks over all CTAs (wave mode)
-  if (!rows && !multi.empty() && int64_t(multi.size()) * 2 <= int64_t(bt->ctx->sms) * lanes) {
+  if (!multi.empty() && int64_t(multi.size()) * 2 <= int64_t(bt->ctx->sms) * lanes) {
     bool ok = true;
     for (int32_t id : multi) ok &= bt->a[size_t(id)] + 1 < 65535;
     if (ok) wave.swap(multi);
@@ -1240,8 +1246,8 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
     size_t pool_used = 0;
     bt->plan_key.clear();
     TA_CK(cudaEventRecord(bt->ev0, st));
-    for (int w = 0; w < 2; ++w) {
-      const std::vector<int32_t>& ids = w ? multi : single;
+    for (int w = 0; w < 3; ++w) {
+      const std::vector<int32_t>& ids = w == 2 ? wave : w ? multi : single;
       if (ids.empty()) continue;
       ++nbuckets;
       size_t pos = 0;
@@ -1268,7 +1274,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
         args.dir_off = bt->d_diroff.ptr;
         BucketLaunch* bl = rows_plan(bt, &pool_used);
         ta::AffEntry ae;
-        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w == 1 ? 1 : 0, st, bl, &ae)) return rc;
+        if (int rc = aff_prepare(bt, chunk, 1, opt.mode, true, w, st, bl, &ae)) return rc;
         if (int rc = aff_launch(bl, ae, args, st, &launches)) return rc;
         bt->stats.padded_cells += bl->padded;
         if (int rc = decode(chunk)) return rc;

@@ -30,7 +30,7 @@ AffEntry affine_kernel_wave(int lanes, int mode, bool trace);
 AffEntry affine_kernel_blocks4(int lanes, int mode);
 
 inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
-  if (blk == 2) return trace ? AffEntry{} : affine_kernel_wave(lanes, mode, false);
+  if (blk == 2) return affine_kernel_wave(lanes, mode, trace);
   return blk ? affine_kernel_blocks(lanes, mode, trace) : affine_kernel_single(lanes, mode, trace);
 }
 
@@ -42,7 +42,6 @@ inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
 #define TA_DEFINE_AFF_TABLE(NAME, BL)                          \
   namespace ta {                                               \
   AffEntry NAME(int lanes, int mode, bool trace) {             \
-    if (trace && BL == 2) return {};                           \
     if (trace) {                                               \
       if (lanes != 1) return {};                               \
       switch (mode) {                                          \

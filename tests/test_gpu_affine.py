@@ -200,3 +200,23 @@ def test_open_zero_equals_linear_on_mixed_block_grids(gpu_engine, mode):
     assert (lin["status"] == 0).all() and (aff["status"] == 0).all()
     bad = np.flatnonzero((lin["score"] != aff["score"]) | (lin["end"] != aff["end"]).any(axis=1))
     assert len(bad) == 0, bad[:10].tolist()
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_wave_traceback_vs_oracle(gpu_engine, oracle, mode):
+    """Few long triplets take wave mode on the rows path too (their blocks
+    spread over all CTAs, linear and affine kernels): score, end, begin and
+    rows equal the oracles'."""
+    rng = np.random.default_rng(31)
+    base = "".join("ACGT"[x] for x in rng.integers(0, 4, size=260))
+    def mutate(s):
+        return "".join(("ACGT"[rng.integers(0, 4)] if rng.random() < 0.08 else c) for c in s if rng.random() > 0.02)
+    trips = [(mutate(base[:230]), mutate(base[:250]), mutate(base[:220])), (mutate(base), mutate(base[:200]), mutate(base))]
+    for sch in ((1, -1, -2, 0), (1, -1, -2, -3)):
+        out = run(trips, sch, mode, rows=True)
+        for x, t in enumerate(trips):
+            want = (oracle.align(t, sch[:3], mode, with_rows=True) if sch[3] == 0
+                    else oracle.affine(t, sch, mode, with_rows=True))
+            got = {"score": int(out["score"][x]), "end": [int(v) for v in out["end"][x]],
+                   "begin": [int(v) for v in out["begin"][x]], "rows": list(out["rows"][x])}
+            assert got == want, (sch, mode, x)
