@@ -1720,36 +1720,83 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   std::vector<int32_t> a(nn), b(nn), c(nn), status(nn, TA_OK);
   std::vector<uint32_t> wofs(3 * nn);
   uint64_t words = 0;
-  for (size_t t = 0; t < nn; ++t) {
-    for (int d = 0; d < 3; ++d) {
-      const int64_t L = offsets[3 * t + d + 1] - offsets[3 * t + d];
-      if (L < 0 || L > (int64_t(1) << 24))
-        return fail(TA_ERR_INVALID_ARGUMENT, "bad sequence offsets for triplet " + std::to_string(t));
-      wofs[3 * t + d] = uint32_t(words);
-      words += uint64_t((L + 15) / 16);
+  int64_t total_cells = 0;
+  // The only O(n) host pass before the first chunk launches (the GPU idles
+  // meanwhile): lengths, packed-word offsets and cells.  Per-triplet checks and
+  // descriptors are made chunk by chunk, behind the previous chunk's kernels.
+  // two parallel passes: per-range lengths / words / cells, then the word
+  // offsets from the ranges' prefix sums
+  {
+    const int nt = int(std::max<size_t>(1, std::min<size_t>(size_t(host_threads()), nn / 32768)));
+    std::vector<uint64_t> rw(size_t(nt) + 1, 0);
+    std::vector<int64_t> rc_(size_t(nt), 0), bad(size_t(nt), -1);
+    auto pass1 = [&](int w) {
+      const size_t t0 = nn * size_t(w) / size_t(nt), t1 = nn * size_t(w + 1) / size_t(nt);
+      uint64_t wd = 0;
+      int64_t cl = 0;
+      for (size_t t = t0; t < t1; ++t) {
+        for (int d = 0; d < 3; ++d) {
+          const int64_t L = offsets[3 * t + d + 1] - offsets[3 * t + d];
+          if ((L < 0 || L > (int64_t(1) << 24)) && bad[size_t(w)] < 0) bad[size_t(w)] = int64_t(t);
+          wd += uint64_t((std::max<int64_t>(L, 0) + 15) / 16);
+        }
+        a[t] = int32_t(offsets[3 * t + 1] - offsets[3 * t]);
+        b[t] = int32_t(offsets[3 * t + 2] - offsets[3 * t + 1]);
+        c[t] = int32_t(offsets[3 * t + 3] - offsets[3 * t + 2]);
+        cl += int64_t(a[t]) * b[t] * c[t];
+      }
+      rw[size_t(w) + 1] = wd;
+      rc_[size_t(w)] = cl;
+    };
+    auto pass2 = [&](int w) {
+      const size_t t0 = nn * size_t(w) / size_t(nt), t1 = nn * size_t(w + 1) / size_t(nt);
+      uint64_t wd = rw[size_t(w)];
+      for (size_t t = t0; t < t1; ++t)
+        for (int d = 0; d < 3; ++d) {
+          wofs[3 * t + d] = uint32_t(wd);
+          wd += uint64_t((std::max<int64_t>(offsets[3 * t + d + 1] - offsets[3 * t + d], 0) + 15) / 16);
+        }
+    };
+    auto run_all = [&](auto&& f) {
+      std::vector<std::thread> pool;
+      for (int w = 1; w < nt; ++w) pool.emplace_back(f, w);
+      f(0);
+      for (auto& th : pool) th.join();
+    };
+    run_all(pass1);
+    for (int w = 0; w < nt; ++w) {
+      if (bad[size_t(w)] >= 0)
+        return fail(TA_ERR_INVALID_ARGUMENT, "bad sequence offsets for triplet " + std::to_string(bad[size_t(w)]));
+      rw[size_t(w) + 1] += rw[size_t(w)];
+      total_cells += rc_[size_t(w)];
     }
-    a[t] = int32_t(offsets[3 * t + 1] - offsets[3 * t]);
-    b[t] = int32_t(offsets[3 * t + 2] - offsets[3 * t + 1]);
-    c[t] = int32_t(offsets[3 * t + 3] - offsets[3 * t + 2]);
+    words = rw[size_t(nt)];
+    if (words > 0xFFFFFFF0ull) return fail(TA_ERR_CAPACITY, "batch exceeds 2^32 packed words");
+    run_all(pass2);
   }
-  if (words > 0xFFFFFFF0ull) return fail(TA_ERR_CAPACITY, "batch exceeds 2^32 packed words");
+  // the batch shim lends lengths and the SM count to plan_streams / prepare_bucket
+  ta_batch shim;
+  shim.ctx = ctx;
   // engine errors per triplet, where the reference raises them (tiled.cpp:8-15, 37-58)
-  for (size_t t = 0; t < nn; ++t) {
-    if (cfg_rc) {
-      status[t] = cfg_rc;
-      continue;
+  auto check = [&](int64_t t0, int64_t t1) {
+    for (int64_t t = t0; t < t1; ++t) {
+      if (cfg_rc) {
+        status[size_t(t)] = cfg_rc;
+        continue;
+      }
+      const int32_t A = shim.a[size_t(t)], B = shim.b[size_t(t)], C = shim.c[size_t(t)];
+      if (uint64_t(A) * uint64_t(B) * uint64_t(C) > opt.cell_budget) {
+        status[size_t(t)] = TA_ERR_CAPACITY;
+        continue;
+      }
+      const int32_t width = opt.team_width > 0 ? opt.team_width : derive_team_width(opt.tile_size, B, C);
+      if (int64_t(width) * opt.tile_size < std::max(B, C)) {
+        status[size_t(t)] = TA_ERR_CONFIG;
+        continue;
+      }
+      if (opt.mode != TA_GLOBAL && !key_fits(A, B, C, scheme)) status[size_t(t)] = TA_ERR_CAPACITY;
     }
-    if (uint64_t(a[t]) * uint64_t(b[t]) * uint64_t(c[t]) > opt.cell_budget) {
-      status[t] = TA_ERR_CAPACITY;
-      continue;
-    }
-    const int32_t width = opt.team_width > 0 ? opt.team_width : derive_team_width(opt.tile_size, b[t], c[t]);
-    if (int64_t(width) * opt.tile_size < std::max(b[t], c[t])) {
-      status[t] = TA_ERR_CONFIG;
-      continue;
-    }
-    if (opt.mode != TA_GLOBAL && !key_fits(a[t], b[t], c[t], scheme)) status[t] = TA_ERR_CAPACITY;
-  }
+  };
   TA_CK(ctx->d_words.reserve(size_t(words) + 2));
   TA_CK(ctx->d_desc.reserve(nn));
   TA_CK(ctx->d_score.reserve(nn));
@@ -1757,11 +1804,7 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   TA_CK(ctx->d_key.reserve(nn));
   TA_CK(ctx->h_desc.reserve(nn));
   TA_CK(ctx->h_out.reserve(4 * nn));
-  for (size_t t = 0; t < nn; ++t)
-    ctx->h_desc.ptr[t] = ta::TripletDesc{a[t], b[t], c[t], 0, wofs[3 * t], wofs[3 * t + 1], wofs[3 * t + 2], 0};
   // chunks: contiguous triplet ranges of ~equal cells
-  int64_t total_cells = 0;
-  for (size_t t = 0; t < nn; ++t) total_cells += int64_t(a[t]) * b[t] * c[t];
   // Chunk boundaries by cells: the first chunks are small (1/64, 1/64, 1/32,
   // 1/16 of the batch) so the GPU starts early; the rest are equal.
   const int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(16, n / 20000));
@@ -1803,11 +1846,6 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   for (auto& e : slot_free) TA_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   TA_CK(cudaEventCreateWithFlags(&h2d_done, cudaEventDisableTiming));
   TA_CK(cudaEventCreateWithFlags(&kdone, cudaEventDisableTiming));
-  TA_CK(cudaMemcpyAsync(ctx->d_desc.ptr, ctx->h_desc.ptr, nn * sizeof(ta::TripletDesc), cudaMemcpyHostToDevice,
-                        ctx->copy));
-  // the batch shim lends lengths and the SM count to plan_streams / prepare_bucket
-  ta_batch shim;
-  shim.ctx = ctx;
   shim.a.swap(a);
   shim.b.swap(b);
   shim.c.swap(c);
@@ -1835,6 +1873,12 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
     TA_CK(cudaEventSynchronize(slot_free[k & 1]));  // the previous H2D from this slot is done
     TA_CK(slot.reserve(size_t(w1 - w0) + 2));
     const auto tp1 = std::chrono::steady_clock::now();
+    check(lo, hi);
+    for (int64_t t = lo; t < hi; ++t)
+      ctx->h_desc.ptr[t] = ta::TripletDesc{shim.a[size_t(t)], shim.b[size_t(t)], shim.c[size_t(t)], 0,
+                                           wofs[3 * size_t(t)], wofs[3 * size_t(t) + 1], wofs[3 * size_t(t) + 2], 0};
+    TA_CK(cudaMemcpyAsync(ctx->d_desc.ptr + lo, ctx->h_desc.ptr + lo, size_t(hi - lo) * sizeof(ta::TripletDesc),
+                          cudaMemcpyHostToDevice, ctx->copy));
     host_pack(seqs, offsets, lo, hi, wofs, w0, slot.ptr, status, threads);
     const auto tp2 = std::chrono::steady_clock::now();
     TA_CK(cudaMemcpyAsync(ctx->d_words.ptr + w0, slot.ptr, size_t(w1 - w0) * 4, cudaMemcpyHostToDevice, ctx->copy));
@@ -1917,12 +1961,21 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
   if (rc != TA_OK) return rc;
   TA_CK(e1);
   TA_CK(e2);
-  for (size_t t = 0; t < nn; ++t) {
-    const bool ok = status[t] == TA_OK;
-    if (out->scores) out->scores[t] = ok ? ctx->h_out.ptr[t] : 0;
-    if (out->ends)
-      for (int d = 0; d < 3; ++d) out->ends[3 * t + d] = ok ? ctx->h_out.ptr[nn + 3 * t + d] : 0;
-    if (out->status) out->status[t] = status[t];
+  auto deliver = [&](size_t t0, size_t t1) {
+    for (size_t t = t0; t < t1; ++t) {
+      const bool ok = status[t] == TA_OK;
+      if (out->scores) out->scores[t] = ok ? ctx->h_out.ptr[t] : 0;
+      if (out->ends)
+        for (int d = 0; d < 3; ++d) out->ends[3 * t + d] = ok ? ctx->h_out.ptr[nn + 3 * t + d] : 0;
+      if (out->status) out->status[t] = status[t];
+    }
+  };
+  {
+    const int nt = int(std::max<size_t>(1, std::min<size_t>(size_t(threads), nn / 65536)));
+    std::vector<std::thread> pool;
+    for (int w = 1; w < nt; ++w) pool.emplace_back(deliver, nn * size_t(w) / size_t(nt), nn * size_t(w + 1) / size_t(nt));
+    deliver(0, nn / size_t(nt));
+    for (auto& th : pool) th.join();
   }
   if (prof) {
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
