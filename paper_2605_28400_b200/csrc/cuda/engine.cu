@@ -565,6 +565,7 @@ struct ta_batch {
   // unchanged (the batch is immutable), so a repeated run does no O(n) host work
   std::string front_key;
   std::vector<int32_t> front_status, front_all_ok;
+  bool status_is_front = false;  // status still equals front_status
   int64_t front_cells = 0;
   int last_mode = -1;
   bool last_rows = false;
@@ -1311,7 +1312,6 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
              ta_results* rows_out) {
   const int64_t n = bt->n;
   bt->stats = ta_stats{};
-  bt->status = bt->pre_status;
   const bool rows = opt.with_rows != 0;
   if (int rc = validate_scheme(scheme)) return rc;
   if (opt.mode < 0 || opt.mode > 2) return fail(TA_ERR_INVALID_ARGUMENT, "unknown alignment mode");
@@ -1334,9 +1334,12 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
   const bool front_hit = front_ok && fkey == bt->front_key && !bt->plan_key.empty();
   if (!front_hit) bt->front_key.clear();
   if (front_hit) {
-    bt->status = bt->front_status;
-    all_ok = bt->front_all_ok;
+    // a repeated run: status and the valid ids are the cached ones (status is
+    // copied back only if another run changed it since)
+    if (!bt->status_is_front) bt->status = bt->front_status;
   } else {
+  bt->status_is_front = false;
+  bt->status = bt->pre_status;
   all_ok.reserve(size_t(n));
   for (int64_t t = 0; t < n; ++t) {
     if (bt->status[size_t(t)] != TA_OK) continue;
@@ -1449,17 +1452,18 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
       lanes_used = std::max(lanes_used, bl->lanes);
       ++nbuckets;
     }
-    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
-      TA_CK(bt->d_ids.reserve(all_ok.size()));
-      TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, all_ok.data(), all_ok.size() * 4, cudaMemcpyHostToDevice, st));
+    const std::vector<int32_t>& ok_ids = front_hit ? bt->front_all_ok : all_ok;
+    if (opt.mode != TA_GLOBAL && !ok_ids.empty()) {
+      TA_CK(bt->d_ids.reserve(ok_ids.size()));
+      TA_CK(cudaMemcpyAsync(bt->d_ids.ptr, ok_ids.data(), ok_ids.size() * 4, cudaMemcpyHostToDevice, st));
     }
     TA_CK(cudaEventRecord(bt->ev0, st));
     for (auto& bl : bt->plan_cache) {
       if (int rc = launch_prepared(bl.get(), base, st, &launches)) return rc;
       bt->stats.padded_cells += bl->padded;
     }
-    if (opt.mode != TA_GLOBAL && !all_ok.empty()) {
-      const int64_t m = int64_t(all_ok.size());
+    if (opt.mode != TA_GLOBAL && !ok_ids.empty()) {
+      const int64_t m = int64_t(ok_ids.size());
       decode_keys_kernel<<<unsigned((m + 255) / 256), 256, 0, st>>>(bt->d_key.ptr, bt->d_desc.ptr, bt->d_ids.ptr, m,
                                                                   bt->d_score.ptr, bt->d_end.ptr);
       TA_CK(cudaGetLastError());
@@ -1634,6 +1638,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
     if (front_ok) {
       bt->front_key = fkey;
       bt->front_status = bt->status;
+      bt->status_is_front = true;
       bt->front_all_ok = all_ok;
       bt->front_cells = cells;
     }
@@ -2212,6 +2217,7 @@ int ta_align_batch(int device, const char* seqs, const int64_t* offsets, int64_t
   if (!bt->rows_scattered)
     TA_CK(cudaMemcpyAsync(rows.data(), bt->d_rows.ptr, size_t(total), cudaMemcpyDeviceToHost, st));
   TA_CK(cudaStreamSynchronize(st));
+  bt->status_is_front = false;
   for (size_t t = 0; t < nn; ++t)
     if (bt->status[t] == TA_OK && dstat[t] != TA_OK) bt->status[t] = dstat[t];
   if (int rc = ta_batch_fetch(bt, out, stream)) return rc;
