@@ -12,6 +12,8 @@ the B200 engine with these files bit for bit.
 Files (tests/golden/parity/):
   C2_global.npz      all 1,000,000 C2 triplets, global: score (end = (a, b, c))
   C2_sample.npz      every 64th C2 triplet, semi-global + local: score, end
+  C2_semi.npz, C2_local.npz   all 1,000,000 C2 triplets, semi-global / local:
+                     score (int16) and end (uint8 x 3)
   C3_sample.npz      every 64th C3 triplet (62,500), all three modes
   C4_sample.npz      every 64th C4 triplet (1,563), all three modes
   C5.npz             1000 / 1500 / 2000 bp single triplets, all three modes
@@ -141,7 +143,7 @@ def main():
         seqs, offs = gen(R, "C5a")
         rows_fixture(L, "C5a", seqs, offs, np.arange(1), os.path.join(OUT, "rows_C5a.json.gz"), threads=1)
 
-    if want("C2") or want("rows_C2") or want("C2_global"):
+    if want("C2") or want("rows_C2") or want("C2_global") or want("C2_full_modes"):
         seqs, offs = gen(R, "C2")
         n = (len(offs) - 1) // 3
         if want("rows_C2"):
@@ -155,6 +157,12 @@ def main():
             assert np.abs(score).max() < 32768
             np.savez_compressed(os.path.join(OUT, "C2_global.npz"), score=score.astype(np.int16))
             log("C2: wrote C2_global.npz")
+        if want("C2_full_modes"):
+            for mode, fname in ((1, "C2_semi.npz"), (2, "C2_local.npz")):
+                score, end = ref_batch(R, seqs, offs, mode)
+                assert np.abs(score).max() < 32768 and end.min() >= 0 and end.max() < 256
+                np.savez_compressed(os.path.join(OUT, fname), score=score.astype(np.int16), end=end.astype(np.uint8))
+                log(f"C2: wrote {fname}")
         del seqs, offs
 
     if want("C3"):

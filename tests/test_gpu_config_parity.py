@@ -3,7 +3,7 @@ of the REFERENCE ITSELF recorded by tests/golden/make_config_parity.py
 (reference run_batch over its tiled engine for scores / ends, reference
 oracle_align for traceback rows).
 
-  C2  all 1,000,000 triplets, global; every 64th triplet, semi-global + local
+  C2  all 1,000,000 triplets in all three modes (and every 64th, semi / local)
   C3  every 64th of 4,000,000 (62,500), all three modes
   C4  every 64th of 100,000 (1,563), all three modes
   C5  1000 / 1500 / 2000 bp single triplets, all three modes (the 2000 bp
@@ -86,6 +86,16 @@ def test_c2_global_all_triplets(gpu_engine):
     assert len(want) == 1000000
     lens = np.diff(offs).reshape(-1, 3).astype(np.int32)
     compare_scores("C2", seqs, offs, 0, want, lens)
+
+
+@pytest.mark.parametrize("mode,fname", [(1, "C2_semi.npz"), (2, "C2_local.npz")])
+def test_c2_semi_local_all_triplets(gpu_engine, mode, fname):
+    """All 1,000,000 C2 triplets in semi-global and local mode (score + end)."""
+    z = np.load(fixture(fname))
+    want_score, want_end = z["score"].astype(np.int32), z["end"].astype(np.int32)
+    assert len(want_score) == 1000000
+    seqs, offs = dataset("C2")
+    compare_scores("C2", seqs, offs, mode, want_score, want_end)
 
 
 @pytest.mark.parametrize("name", ["C2", "C3", "C4"])

@@ -269,3 +269,31 @@ def test_device_batch_rerun_cache(gpu_engine):
     assert (b.fetch()["status"] != 0).all()
     b.run(ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(0), ta.EngineConfig(cell_budget=1 << 40))
     assert (b.fetch()["status"] == 0).all()
+
+
+def test_one_shot_statuses_across_chunks(gpu_engine):
+    """The pipelined one-shot path (ta_align_batch, ~10 chunks here) checks
+    and packs each chunk behind the previous chunk's kernels: per-triplet
+    statuses (non-ACGT residues, cell budget) and results must equal the
+    resident-batch path's on the same inputs; malformed offsets fail the call."""
+    seqs, offs = ta.generate("uniform:20:150:200000", 0.05, 0.01, 23)
+    seqs = seqs.copy()
+    n = (len(offs) - 1) // 3
+    for t in (5, 77777, 150001, n - 1):  # a residue 'N' in four chunks
+        seqs[offs[3 * t + 1]] = ord("N")
+    lens = np.diff(offs).reshape(-1, 3).astype(np.int64)
+    budget = int(np.percentile(np.prod(lens, axis=1), 90))  # ~10% capacity errors
+    for mode in (0, 1):
+        cfg = ta.EngineConfig(cell_budget=budget)
+        got = ta.align_arrays(seqs, offs, ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(mode), cfg=cfg)
+        b = ta.DeviceBatch(seqs, offs)
+        b.run(ta.ScoringScheme(1, -1, -2), ta.AlignmentMode(mode), cfg)
+        want = b.fetch()
+        assert (got["status"] == want["status"]).all(), mode
+        assert (got["score"] == want["score"]).all() and (got["end"] == want["end"]).all(), mode
+        assert int((got["status"] != 0).sum()) > n // 20
+        assert all(int(got["status"][t]) != 0 for t in (5, 77777, 150001, n - 1))
+    bad = offs.copy()
+    bad[3 * 1000 + 1] = bad[3 * 1000] - 1  # a negative length
+    with pytest.raises(Exception):
+        ta.align_arrays(seqs, bad, ta.ScoringScheme(1, -1, -2), ta.AlignmentMode.Global)
