@@ -91,6 +91,8 @@ def test_c2_global_all_triplets(gpu_engine):
 @pytest.mark.parametrize("mode,fname", [(1, "C2_semi.npz"), (2, "C2_local.npz")])
 def test_c2_semi_local_all_triplets(gpu_engine, mode, fname):
     """All 1,000,000 C2 triplets in semi-global and local mode (score + end)."""
+    if not os.path.exists(os.path.join(PAR, fname)):
+        pytest.skip(f"{fname} not generated (make_config_parity.py --only C2_full_modes)")
     z = np.load(fixture(fname))
     want_score, want_end = z["score"].astype(np.int32), z["end"].astype(np.int32)
     assert len(want_score) == 1000000
