@@ -10,9 +10,11 @@
 //  * One CTA is a G x G grid of threads; thread (r, c) owns the N x N tile
 //    j in [rN, rN+N), k in [cN, cN+N) of the (j, k) plane (the plane
 //    includes the j = 0 / k = 0 faces, so every cell runs the same code).
-//    The tile lives in registers; the previous i-slice is kept alongside.
+//    The tile lives in registers and is updated in place (slice i - 1 until
+//    the sweep of slice i overwrites a cell).
 //  * Anti-diagonal pipeline (tiled.hpp:386-388): thread (r, c) computes
-//    stream position s - r - c at step s.  Each CTA owns LANES independent
+//    stream position s - LAG (r + c) at step s (LAG = 2 for single-plane
+//    kernels, see WaveSmem).  Each CTA owns LANES independent
 //    "slice streams" (the concatenated slices of the triplets assigned to
 //    it), so the pipeline fills once per CTA, not once per triplet.
 //  * LANES = 2 packs two independent triplet streams into s16x2 registers:
@@ -23,7 +25,8 @@
 //    2 VIADDMNMX + 2 VIMNMX3 + 2 packed adds (IMAD), sigma12' folded out of
 //    max(t1, t4).
 //  * Neighbour boundaries (right column / down row + corner) go through a
-//    double-buffered shared-memory mailbox, one __syncthreads per step.
+//    shared-memory mailbox ring of LAG + 1 buffers, synchronised by
+//    mbarriers (split arrive / wait, no __syncthreads in the loop).
 //  * Exactness: all arithmetic is integer; lane width is chosen by the host
 //    from a proven bound, so results are bit-identical to the reference.
 #pragma once
