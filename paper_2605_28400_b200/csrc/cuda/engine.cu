@@ -8,6 +8,7 @@
 // There is no CPU fallback: every alignment is computed by the kernels in
 // wavefront.cuh; a missing/failed device is reported as TA_ERR_CUDA.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a profiler attaches
 
 #include <algorithm>
 #include <atomic>
@@ -28,6 +29,17 @@
 #include "../../../include/trioalign_capi.h"
 #include "kernels.h"
 #include "kernels_aff.h"
+
+namespace {
+// NVTX range for the host phases of the engine (visible in Nsight Systems /
+// Compute timelines: ta/create, ta/plan, ta/launch, ta/rows, ...)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 namespace {
 
@@ -1134,6 +1146,7 @@ int aff_launch(BucketLaunch* bl, const ta::AffEntry& ae, const ta::AffArgs& base
 
 int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
                const std::vector<int32_t>& all_ok, bool rows) {
+  NvtxRange nv(rows ? "ta/affine_rows" : "ta/affine");
   const int64_t n = bt->n;
   std::vector<int32_t> single, multi, wave;
   int64_t maxb = 0;
@@ -1310,6 +1323,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
 
 int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaStream_t st,
              ta_results* rows_out) {
+  NvtxRange nv(opt.with_rows ? "ta/run_rows" : "ta/run");
   const int64_t n = bt->n;
   bt->stats = ta_stats{};
   const bool rows = opt.with_rows != 0;
@@ -1715,6 +1729,7 @@ void host_pack(const char* seqs, const int64_t* offs, int64_t lo, int64_t hi, co
 
 int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offsets, int64_t n,
                            const ta_scheme& scheme, const ta_options& opt, ta_results* out, cudaStream_t st) {
+  NvtxRange nv("ta/align_pipelined");
   std::lock_guard<std::mutex> lock(ctx->mu);
   const auto tq0 = std::chrono::steady_clock::now();
   if (int rc = validate_scheme(scheme)) return rc;
@@ -2097,6 +2112,7 @@ static int batch_init(ta_batch* bt, DeviceCtx* ctx, int device, const char* seqs
 
 int ta_batch_create(int device, const char* seqs, const int64_t* offsets, int64_t n,
                     ta_batch** out, void* stream) {
+  NvtxRange nv("ta/batch_create");
   *out = nullptr;
   if (n < 0) return fail(TA_ERR_INVALID_ARGUMENT, "negative triplet count");
   DeviceCtx* ctx = nullptr;
@@ -2121,6 +2137,7 @@ int ta_batch_run(ta_batch* b, const ta_scheme* scheme, const ta_options* opt, vo
 }
 
 int ta_batch_fetch(ta_batch* b, ta_results* out, void* stream) {
+  NvtxRange nv("ta/batch_fetch");
   if (!b || !out) return fail(TA_ERR_INVALID_ARGUMENT, "null argument");
   TA_CK(cudaSetDevice(b->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : b->ctx->stream;
