@@ -62,7 +62,7 @@ OPS_PER_CELL = 13          # 7 add + 6 max per interior cell
 INT_LANES_PER_CLK_SM = 64  # measured: VIADDMNMX/VIMNMX3 issue rate (profiles/r01_intpeak.jsonl)
 SMS = 148
 AFFINE_OPEN = -3           # gap_open of the affine line (SPEC-AFFINE.md)
-AFFINE_ALU_PER_CELL = 16   # ALU-pipe instructions per cell-lane of affine.cuh (SASS: VIADDMNMX + VIMNMX3)
+AFFINE_ALU_PER_CELL = 14   # ALU-pipe instructions per cell-lane of affine.cuh (SASS: VIADDMNMX + VIMNMX3)
 AFFINE_OPS_PER_CELL = 39   # SPEC-AFFINE.md "Algorithmic work": algorithmic int ops per affine cell
 ROWS_CPU_SAMPLE = 200      # C1 triplets timed through the reference oracle_align (1 core)
 

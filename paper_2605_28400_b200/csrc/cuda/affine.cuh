@@ -20,7 +20,7 @@
 // (primes: previous slice).  A thread keeps B, E2, E3, E5 of its tile for the
 // next slice and E4, E6, E7 for the cells to its right / below; the mailbox
 // carries (B, E3, E4, E7) of the right column and (B, E4, E2, E6) of the bottom
-// row.  16 ALU-pipe (VIADDMNMX / VIMNMX3) + 10 FMA-pipe (IMAD) instructions
+// row.  14 ALU-pipe (VIADDMNMX / VIMNMX3) + 8 FMA-pipe (IMAD) instructions
 // per cell; values are gap-shifted (-2 gap (i+j+k)) and biased by -10 open so
 // that every real value is >= 0 and packed s16x2 adds on the FMA pipe are
 // exact.  TRACE: values carry a 3-bit type tag (7 - t) in their low bits, the
@@ -608,16 +608,24 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               v7 = v7 & ~7u;
             }
             const uint32_t b = Ops::max3(Ops::max3(Ops::max3(v1, v2, v3), v4, v5), v6, v7);
+            // E_t = max(V_t, open + V_a, open + V_b, 2 open + B) ({a, b}: the
+            // n = 1 types of t).  Every E_t takes b2, and every open + V_a
+            // appears in two E_t, so four of them are fused with b2 once
+            // (p_a = max(V_a + open, b2), one VIADDMNMX) and each E_t is one
+            // VIMNMX3 of three shared terms: 10 ALU + 2 FMA for the six E_t
+            // instead of 12 + 4; the candidate sets, hence the (tagged)
+            // maxima, are unchanged.
             const uint32_t b2 = fma_add(b, one, osub2);
-            const uint32_t w2 = fma_add(v2, one, osub1), w3 = fma_add(v3, one, osub1);
-            const uint32_t w5 = fma_add(v5, one, osub1), w6 = fma_add(v6, one, osub1);
+            const uint32_t p2 = Ops::addmax(v2, op1, b2), p4 = Ops::addmax(v4, op1, b2);
+            const uint32_t p5 = Ops::addmax(v5, op1, b2), p7 = Ops::addmax(v7, op1, b2);
+            const uint32_t w3 = fma_add(v3, one, osub1), w6 = fma_add(v6, one, osub1);
             cB[P][Q] = b;
-            cE2[P][Q] = Ops::addmax(v6, op1, Ops::max3(v2, w5, b2));
-            cE3[P][Q] = Ops::addmax(v7, op1, Ops::max3(v3, w5, b2));
-            cE4[P][Q] = Ops::addmax(v7, op1, Ops::max3(v4, w6, b2));
-            cE5[P][Q] = Ops::addmax(v3, op1, Ops::max3(v5, w2, b2));
-            cE6[P][Q] = Ops::addmax(v4, op1, Ops::max3(v6, w2, b2));
-            cE7[P][Q] = Ops::addmax(v4, op1, Ops::max3(v7, w3, b2));
+            cE2[P][Q] = Ops::max3(v2, p5, w6);  // v2, open + v5, open + v6, b2
+            cE3[P][Q] = Ops::max3(v3, p5, p7);  // v3, open + v5, open + v7, b2
+            cE4[P][Q] = Ops::max3(v4, w6, p7);  // v4, open + v6, open + v7, b2
+            cE5[P][Q] = Ops::max3(v5, p2, w3);  // v5, open + v2, open + v3, b2
+            cE6[P][Q] = Ops::max3(v6, p2, p4);  // v6, open + v2, open + v4, b2
+            cE7[P][Q] = Ops::max3(v7, w3, p4);  // v7, open + v3, open + v4, b2
             if constexpr (TRACE) rec[cell] = rc | ((b & 7u) << 3);
           }
         }
