@@ -550,24 +550,28 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
       const uint32_t ag2s = Ops::splat(ag2 * SC);
 
       // ---- 4. the tile -------------------------------------------------------
+      // Cells in anti-diagonal order (d = P + Q), as in the linear sweep:
+      // consecutive cells are independent, so the E7 -> B -> E7 chain along a
+      // row and E6 along a column are several cells apart in the schedule.
       auto sweep = [&]() {
-        uint32_t strow = stbase;
-        [[maybe_unused]] uint32_t frv = frb, fcv = fcb;
+        [[maybe_unused]] uint32_t sd = stbase;  // local: start value of diagonal d (depends on P + Q only)
+        [[maybe_unused]] uint32_t frv = frb, fcv = fcb;  // semi: row-1 cells come with Q, column-1 cells with P increasing
 #pragma unroll
-        for (int P = 1; P <= N; ++P) {
-          [[maybe_unused]] uint32_t st = strow;
+        for (int d = 0; d <= 2 * N - 2; ++d) {
           if constexpr (MODE == kLocal) {
-            if (P < N) strow = fma_add(strow, one, ag2s);
+            if (d > 0) sd = fma_add(sd, one, ag2s);
           }
 #pragma unroll
-          for (int Q = 1; Q <= N; ++Q) {
+          for (int P0 = 0; P0 < N; ++P0) {
+            const int Q0 = d - P0;
+            if (Q0 < 0 || Q0 >= N) continue;
+            const int P = P0 + 1, Q = Q0 + 1;
             const int cell = (P - 1) * N + (Q - 1);
             const uint32_t sg = s12w[cell * T + t];
             // start value of this cell (NEG where no alignment may start)
             uint32_t start = NEG;
             if constexpr (MODE == kLocal) {
-              start = st;
-              if (Q < N) st = fma_add(st, one, ag2s);
+              start = sd;
             } else {
               if (P == 1 && Q == 1) start = fcorner;
               if constexpr (MODE == kSemi) {
@@ -587,7 +591,11 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
             if (P < N && Q < N) Y[P + 1][Q + 1] = fma_add(fma_add(oB, one, a1v[P]), one, s02[Q]);
             if (P < N) V2[P + 1][Q] = fma_add(oE2, one, a1v[P]);
             if (Q < N) V3[P][Q + 1] = fma_add(oE3, one, s02[Q]);
-            uint32_t v1 = Ops::addmax(Y[P][Q], sg, start);
+            // no start possible here (global: all but the origin cell; semi:
+            // off row / column 1): V1 is a plain packed add on the FMA pipe
+            // (Y >= NEG-derived, sg >= 0: the clamp at NEG never binds)
+            const bool no_start = MODE == kGlobal ? (P > 1 || Q > 1) : MODE == kSemi ? (P > 1 && Q > 1) : false;
+            uint32_t v1 = no_start ? fma_add(Y[P][Q], one, sg) : Ops::addmax(Y[P][Q], sg, start);
             uint32_t v2 = V2[P][Q];
             uint32_t v3 = V3[P][Q];
             uint32_t v4 = fma_add(cE4[P - 1][Q - 1], one, sg);
