@@ -248,6 +248,12 @@ __device__ __forceinline__ int base_at(const uint32_t* __restrict__ seq, uint32_
   return static_cast<int>((__ldg(seq + w + (pos >> 4)) >> ((pos & 15) * 2)) & 3u);
 }
 
+#ifdef TA_WAVE_CLOCK
+// dev-only (variant builds): per wave CTA and step, globaltimer at the step
+// start, after the faces were taken and at the mailbox arrival (thread 0)
+static __device__ unsigned long long g_wave_clock[4096][256][8];  // CTA 1 only, every thread
+#endif
+
 template <int N, int G, int LANES, int BLK = 1>
 struct WaveSmem {
   static constexpr int T = G * G;
@@ -273,8 +279,9 @@ struct WaveSmem {
   static constexpr size_t kSig = size_t(NN) * T * 4;      // sigma12 per cell
   static constexpr size_t kTab = size_t(N) * T * 8;       // per table (8 B per (row, thread))
   static constexpr size_t kX = size_t(NB) * XW * (T + 1) * 4;
-  // cold per-lane state: single-plane kernels keep no block geometry
-  static constexpr int kLaneFields = BLK ? 10 : 6;
+  // cold per-lane state: single-plane kernels keep no block geometry, wave
+  // kernels also the ring base (kWSeg)
+  static constexpr int kLaneFields = BLK == 2 ? 11 : BLK ? 10 : 6;
   static constexpr size_t kLane = size_t(LANES) * kLaneFields * T * 4;
   // prefetched block faces (either layout); single-plane kernels have none
   static constexpr size_t kStage = BLK ? size_t(LANES) * 2 * G * kSegE * 8 : 0;
@@ -289,7 +296,9 @@ struct WaveSmem {
 
 // Cold per-lane fields kept in shared memory ([lane][field][thread]); the
 // block geometry (kOrgJ ..) is stored by block kernels only (constants else).
-enum LaneField { kItem = 0, kTid, kLenB, kLenC, kW0, kLen, kOrgJ, kOrgK, kBk, kBj, kIEnd };  // kIEnd: affine kernel only
+enum LaneField { kItem = 0, kTid, kLenB, kLenC, kW0, kLen, kOrgJ, kOrgK, kBk, kBj, kIEnd, kWSeg = kIEnd };
+// kIEnd: affine kernel only; kWSeg: linear wave kernels only - the block's own ring base in kSegE-entry
+// segments, so face addresses need no dependent global load of wave_base per step
 
 // ---------------------------------------------------------------------------
 template <int N, int G, int LANES, int MODE, bool TRACE, int BLK>
@@ -455,6 +464,13 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     LS(l, kLen) = len;
     LS(l, kBk) = Bk;
     LS(l, kBj) = Bj;
+    if constexpr (WAVE) {
+      // ring bases are multiples of kSegE entries (wave_block_entries); 2^32
+      // segments of 96 B exceed the device memory
+      LS(l, kWSeg) = id >= 0 ? static_cast<int32_t>(static_cast<uint32_t>(
+                                   args.wave_base[id] / kSegE + int64_t(J * Bk + K) * 2 * (a_ + 1) * G))
+                             : 0;
+    }
     const int gj0 = J * GN + j0, gk0 = K * GN + k0;
     uint32_t f = (id >= 0 || it < iend) ? 0u : kDone;  // a null item keeps the lane alive
     if (id >= 0 && b_ / N == gj0 / N && c_ / N == gk0 / N && b_ >= gj0 && c_ >= gk0) f |= kOwner;
@@ -634,8 +650,38 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
       if (s_ >= 1) wait_step(s_ - 1);
     }
   };
+  // Wave mode: segment `idx` of slice `sl` of ring `ring` (0 down, 1 right) of
+  // the block at offset `dblk` from this lane's (0 own, -1 left, -Bk top)
+  [[maybe_unused]] auto ring_seg = [&](int l, int dblk, int ring, int sl, int idx) -> uint64_t* {
+    const int a1 = la[l] + 1;
+    const int64_t seg = int64_t(static_cast<uint32_t>(LS(l, kWSeg))) + ((int64_t(dblk) * 2 + ring) * a1 + sl) * G + idx;
+    return reinterpret_cast<uint64_t*>(args.faces) + seg * kSegE;
+  };
+  // Wave mode: stage the (value, tag) face segments of slice `sl` of lane l
+  // (cp.async, no registers held).  A step issues the next slice's segments
+  // right after it has read this slice's, so the L2 round trip from the
+  // producer CTA overlaps the whole sweep instead of the next step's start.
+  [[maybe_unused]] auto wave_prefetch = [&](int l, int sl) {
+    if (LS(l, kTid) < 0 || !(flags[l] & (kInTop | kInLeft))) return;
+    auto fetch_seg = [&](int seg, const uint64_t* src) {
+      uint64_t* dst = reinterpret_cast<uint64_t*>(stage) + (l * 2 * G + seg) * kSegE;
+#pragma unroll
+      for (int v = 0; v < kSegE / 2; ++v)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(dst + 2 * v))),
+                     "l"(src + 2 * v)
+                     : "memory");
+    };
+    if (r == 0 && (flags[l] & kInTop))  // down ring of block (J - 1, K), segment cc
+      fetch_seg(cc, ring_seg(l, -LS(l, kBk), 0, sl, cc));
+    if (cc == 0 && (flags[l] & kInLeft))  // right ring of block (J, K - 1), segment r
+      fetch_seg(G + r, ring_seg(l, -1, 1, sl, r));
+  };
   for (int s = 0; s < nsteps; ++s) {
     const int buf = s % NB;
+    [[maybe_unused]] bool early[LANES];
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) early[l] = false;
     const int rbuf = (s + 1) % NB;  // == (s - LAG) mod NB
     bool any = false;
 #pragma unroll
@@ -643,7 +689,21 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
     const bool active = s >= skew && any;
     // Every thread (active or idle) waits for the previous phase before it
     // arrives again: no thread can arrive on mbar[b] twice within one phase.
+#ifdef TA_WAVE_CLOCK
+    auto wclock = [&](int k) {
+      if (WAVE && blockIdx.x == 1 && s < 4096 && T <= 256) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        g_wave_clock[s][r * G + cc][k] = g;
+      }
+    };
+    wclock(0);
+    unsigned long long wrereads = 0;
+#endif
     if (s >= LAG) wait_step(s - LAG);
+#ifdef TA_WAVE_CLOCK
+    wclock(3);
+#endif
     // A tile that holds no real cell of any live lane this step (padding
     // beyond b / c, or the padded slices of a block item) skips the sweep: its
     // values only ever feed other padding, and its warp's issue slots go to
@@ -756,6 +816,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
         if (top || lft) {
           asm volatile("cp.async.wait_all;" ::: "memory");
+#ifdef TA_WAVE_CLOCK
+          wclock(5);
+#endif
           if (kPackFaces && paired) {
             if (r == 0 && (flags[0] & kInTop) && si[0] <= la[0]) {
               const uint32_t* st = reinterpret_cast<const uint32_t*>(stage) + cc * (N + 1);
@@ -774,30 +837,61 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
             if constexpr (WAVE) {
               if (LS(l, kTid) < 0) continue;  // a null item (idle partner lane) has no faces
               const uint32_t want = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
-              const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
-              const int a1 = la[l] + 1;
-              const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
-              // staged (value, tag) entry e of segment seg; re-read from L2 until fresh
-              auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
-                uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kSegE + e];
-                while (v.y != want) {
-                  v = ld_face(src + e);
+              // the staged (value, tag) entries [0, CNT) of segment seg: one
+              // branch when every tag is fresh (the common case); otherwise
+              // each stale entry is re-read from L2 until its tag matches
+              auto take_seg = [&](int seg, const uint64_t* src, auto cnt, int32_t (&out)[N + 1]) {
+                constexpr int CNT = decltype(cnt)::value;
+                const uint2* sv = reinterpret_cast<const uint2*>(stage) + (l * 2 * G + seg) * kSegE;
+                uint2 v[CNT];
+                bool fresh = true;
+#pragma unroll
+                for (int e = 0; e < CNT; ++e) {
+                  v[e] = sv[e];
+                  fresh &= v[e].y == want;
                 }
-                return static_cast<int32_t>(v.x);
+                if (!fresh) {
+#pragma unroll
+                  for (int e = 0; e < CNT; ++e) {
+                    uint2 w = v[e];
+                    while (w.y != want) {
+                      w = ld_face(src + e);
+#ifdef TA_WAVE_CLOCK
+                      ++wrereads;
+#endif
+                    }
+                    out[e] = static_cast<int32_t>(w.x);
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < CNT; ++e) out[e] = static_cast<int32_t>(v[e].x);
+                }
               };
               // only a lane for which this tile holds real cells waits for its
               // faces: padding producers of the other lane skip their sweep
               const bool real = LS(l, kLenB) - LS(l, kOrgJ) - j0 >= 0 && LS(l, kLenC) - LS(l, kOrgK) - k0 >= 0;
               if (r == 0 && (flags[l] & kInTop) && ok && real) {
-                const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kSegE;
+                int32_t fv[N + 1];
+                take_seg(cc, ring_seg(l, -LS(l, kBk), 0, si[l], cc), std::integral_constant<int, N + 1>{}, fv);
 #pragma unroll
-                for (int q = 0; q <= N; ++q) Cu[0][q] = lop_sel(Cu[0][q], Ops::splat(take(cc, src, q) << SH), Ops::mask(l));
+                for (int q = 0; q <= N; ++q) Cu[0][q] = lop_sel(Cu[0][q], Ops::splat(fv[q] << SH), Ops::mask(l));
               }
               if (cc == 0 && (flags[l] & kInLeft) && ok && real) {
-                const uint64_t* src = fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE;
+                int32_t fv[N + 1];
+                take_seg(G + r, ring_seg(l, -1, 1, si[l], r), std::integral_constant<int, N>{}, fv);
 #pragma unroll
-                for (int p = 0; p < N; ++p)
-                  Cu[p + 1][0] = lop_sel(Cu[p + 1][0], Ops::splat(take(G + r, src, p) << SH), Ops::mask(l));
+                for (int p = 0; p < N; ++p) Cu[p + 1][0] = lop_sel(Cu[p + 1][0], Ops::splat(fv[p] << SH), Ops::mask(l));
+              }
+              // this lane's staged segments are consumed: stage the next slice
+              if (!(flags[l] & kDone) && si[l] + 1 <= la[l]) {
+#ifdef TA_WAVE_CLOCK
+                wclock(6);
+#endif
+                wave_prefetch(l, si[l] + 1);
+#ifdef TA_WAVE_CLOCK
+                wclock(7);
+#endif
+                early[l] = true;
               }
               continue;
             }
@@ -815,6 +909,12 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
       }
 
+#ifdef TA_WAVE_CLOCK
+      wclock(1);
+      {
+        if (WAVE && blockIdx.x == 1 && s < 4096 && T <= 256) g_wave_clock[s][r * G + cc][4] = wrereads;
+      }
+#endif
       // ---- 3. forced cells (reference initialisation, oracle.cpp:30-39) --
       // global: M(0,0,0) = 0; semi: axis cells are 0 in M-space.
       uint32_t fcorner = NEG;
@@ -995,15 +1095,13 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
           const int a1 = la[l] + 1;
           if constexpr (WAVE) {
             const uint32_t tag = (args.epoch << 16) + static_cast<uint32_t>(si[l]) + 1u;
-            uint64_t* fb = reinterpret_cast<uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
-            const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
             if (dn) {  // down ring of this block: segment cc, entries q = 0..N (q = 0 is the corner)
-              uint2* d = reinterpret_cast<uint2*>(fb + ((int64_t(blk) * 2 * a1 + si[l]) * G + cc) * kSegE);
+              uint2* d = reinterpret_cast<uint2*>(ring_seg(l, 0, 0, si[l], cc));
 #pragma unroll
               for (int q = 0; q <= N; ++q) st_face(d + q, static_cast<uint32_t>(Ops::lane(Cu[N][q], l) >> SH), tag);
             }
             if (rt) {  // right ring: segment r, entries p = 0..N-1
-              uint2* d = reinterpret_cast<uint2*>(fb + (((int64_t(blk) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
+              uint2* d = reinterpret_cast<uint2*>(ring_seg(l, 0, 1, si[l], r));
 #pragma unroll
               for (int p = 0; p < N; ++p) st_face(d + p, static_cast<uint32_t>(Ops::lane(Cu[p + 1][N], l) >> SH), tag);
             }
@@ -1040,6 +1138,9 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         }
         if (wrote) __threadfence_block();
       }
+#ifdef TA_WAVE_CLOCK
+      wclock(2);
+#endif
       mbar_arrive_group(&mbar[buf]);
 
       // ---- 7. score extraction ------------------------------------------
@@ -1319,22 +1420,7 @@ __global__ void __launch_bounds__(G * G, 1) wavefront_kernel(const WaveArgs args
         if ((flags[l] & kDone) || si[l] > la[l]) continue;
         const int a1 = la[l] + 1;
         if constexpr (WAVE) {
-          if (LS(l, kTid) < 0 || !(flags[l] & (kInTop | kInLeft))) continue;
-          const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.wave_base[LS(l, kTid)];
-          const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
-          auto fetch_seg = [&](int seg, const uint64_t* src) {
-            uint64_t* dst = reinterpret_cast<uint64_t*>(stage) + (l * 2 * G + seg) * kSegE;
-#pragma unroll
-            for (int v = 0; v < kSegE / 2; ++v)
-              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                               static_cast<uint32_t>(__cvta_generic_to_shared(dst + 2 * v))),
-                           "l"(src + 2 * v)
-                           : "memory");
-          };
-          if (r == 0 && (flags[l] & kInTop))  // down ring of block (J - 1, K), segment cc
-            fetch_seg(cc, fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kSegE);
-          if (cc == 0 && (flags[l] & kInLeft))  // right ring of block (J, K - 1), segment r
-            fetch_seg(G + r, fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kSegE);
+          if (!early[l]) wave_prefetch(l, si[l]);  // else issued right after this step's halos
           continue;
         }
         if (kPackFaces && paired && l != 0) continue;  // packed faces: lane 0's buffer only
