@@ -442,36 +442,60 @@ __global__ void __launch_bounds__(G * G, 1) affine_kernel(const AffArgs args) {
               const uint64_t* fb = reinterpret_cast<const uint64_t*>(args.faces) + args.face_off[LS(l, kTid)];
               const int a1 = la[l] + 1;
               const int blk = (LS(l, kOrgJ) / GN) * LS(l, kBk) + LS(l, kOrgK) / GN;
+              const uint2* sv = reinterpret_cast<const uint2*>(stage) + l * 2 * G * kAffSegE;
+              // staged entry e of segment seg, re-read from L2 until its tag is fresh
               auto take = [&](int seg, const uint64_t* src, int e) -> int32_t {
-                uint2 v = reinterpret_cast<const uint2*>(stage)[(l * 2 * G + seg) * kAffSegE + e];
+                uint2 v = sv[seg * kAffSegE + e];
                 while (v.y != want) {
                   v = ld_face(src + e);
                 }
                 return static_cast<int32_t>(v.x);
               };
-              if (r == 0 && (flags[l] & kInTop)) {
-                const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kAffSegE;
+              // entries a segment's consumer reads: top (B, E4) at q < N, (E2, E6) at q > 0; left all 4N
+              auto used = [](bool top, int e) { return !top || (e % 2 == 0 ? e < 4 * N : e >= 4); };
+              // one branch when every used tag is fresh (the common case: see wavefront.cuh)
+              auto fresh = [&](int seg, bool top) {
+                bool f = true;
+#pragma unroll
+                for (int e = 0; e < 4 * N + 4; ++e)
+                  if (e < (top ? 4 * N + 4 : 4 * N) && used(top, e)) f &= sv[seg * kAffSegE + e].y == want;
+                return f;
+              };
+              auto put_top = [&](auto get) {
 #pragma unroll
                 for (int q = 0; q <= N; ++q) {  // (B, E2, E4, E6) at k = cN + q - 1
                   if (q < N) {
-                    cB[0][q] = lop_sel(cB[0][q], Ops::splat(take(cc, src, 4 * q)), m);
-                    cE4[0][q] = lop_sel(cE4[0][q], Ops::splat(take(cc, src, 4 * q + 2)), m);
+                    cB[0][q] = lop_sel(cB[0][q], Ops::splat(get(4 * q)), m);
+                    cE4[0][q] = lop_sel(cE4[0][q], Ops::splat(get(4 * q + 2)), m);
                   }
                   if (q > 0) {
-                    cE2[0][q] = lop_sel(cE2[0][q], Ops::splat(take(cc, src, 4 * q + 1)), m);
-                    cE6[0][q] = lop_sel(cE6[0][q], Ops::splat(take(cc, src, 4 * q + 3)), m);
+                    cE2[0][q] = lop_sel(cE2[0][q], Ops::splat(get(4 * q + 1)), m);
+                    cE6[0][q] = lop_sel(cE6[0][q], Ops::splat(get(4 * q + 3)), m);
                   }
                 }
+              };
+              auto put_left = [&](auto get) {
+#pragma unroll
+                for (int p = 0; p < N; ++p) {  // (B, E3, E4, E7) at j = rN + p
+                  cB[p + 1][0] = lop_sel(cB[p + 1][0], Ops::splat(get(4 * p)), m);
+                  cE3[p + 1][0] = lop_sel(cE3[p + 1][0], Ops::splat(get(4 * p + 1)), m);
+                  cE4[p + 1][0] = lop_sel(cE4[p + 1][0], Ops::splat(get(4 * p + 2)), m);
+                  cE7[p + 1][0] = lop_sel(cE7[p + 1][0], Ops::splat(get(4 * p + 3)), m);
+                }
+              };
+              if (r == 0 && (flags[l] & kInTop)) {
+                const uint64_t* src = fb + ((int64_t(blk - LS(l, kBk)) * 2 * a1 + si[l]) * G + cc) * kAffSegE;
+                if (fresh(cc, true))
+                  put_top([&](int e) { return static_cast<int32_t>(sv[cc * kAffSegE + e].x); });
+                else
+                  put_top([&](int e) { return take(cc, src, e); });
               }
               if (cc == 0 && (flags[l] & kInLeft)) {
                 const uint64_t* src = fb + (((int64_t(blk - 1) * 2 + 1) * a1 + si[l]) * G + r) * kAffSegE;
-#pragma unroll
-                for (int p = 0; p < N; ++p) {  // (B, E3, E4, E7) at j = rN + p
-                  cB[p + 1][0] = lop_sel(cB[p + 1][0], Ops::splat(take(G + r, src, 4 * p)), m);
-                  cE3[p + 1][0] = lop_sel(cE3[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 1)), m);
-                  cE4[p + 1][0] = lop_sel(cE4[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 2)), m);
-                  cE7[p + 1][0] = lop_sel(cE7[p + 1][0], Ops::splat(take(G + r, src, 4 * p + 3)), m);
-                }
+                if (fresh(G + r, false))
+                  put_left([&](int e) { return static_cast<int32_t>(sv[(G + r) * kAffSegE + e].x); });
+                else
+                  put_left([&](int e) { return take(G + r, src, e); });
               }
               continue;
             }
