@@ -869,6 +869,18 @@ void split_largest(const std::vector<int32_t>& bucket, const std::vector<int32_t
   *lanes8 = s16_ok(scheme, bound8) ? 2 : 1;
 }
 
+// Tile side of score-only wave buckets: a wave step is latency bound per
+// thread, so the 8 x 8 tiles (64 cells per tile-step instead of 100) shorten
+// every step of a long triplet's critical path.  TA_WAVE_TILE=10 selects the
+// 10 x 10 kernels (dev-only A/B knob).
+int wave_tile_n() {
+  static const int n = [] {
+    const char* e = std::getenv("TA_WAVE_TILE");
+    return e && std::atoi(e) == ta::kTileN ? ta::kTileN : ta::kSmallTileN;
+  }();
+  return n;
+}
+
 // Host planning + upload for one bucket (outside any timed region).
 int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int lanes, int mode,
                    bool trace, cudaStream_t st, BucketLaunch* bl, bool wave = false, int tile_n = ta::kTileN) {
@@ -877,7 +889,20 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
   bl->mode = mode;
   bl->wave = wave;
   if (wave) {
-    bl->ke = ta::lookup_kernel(grid, lanes, mode, trace, 2);
+    // the lane width was proven for 160-wide blocks: keep 8 x 8 tiles only
+    // while no triplet's 128-padded extents exceed its 160-padded ones (the
+    // value bound grows with them, lane_bound)
+    for (int32_t id : ids) {
+      if (tile_n == ta::kTileN) break;
+      auto ext = [&](int n) {
+        const int64_t gn = int64_t(grid) * n;
+        return ((bt->b[size_t(id)] + gn) / gn + (bt->c[size_t(id)] + gn) / gn) * gn;
+      };
+      if (ext(tile_n) > ext(ta::kTileN)) tile_n = ta::kTileN;
+    }
+    if (tile_n != ta::kTileN && (grid != 16 || trace))
+      return fail(TA_ERR_LOGIC, "8 x 8-tile wave kernels exist for score items of grid 16 only");
+    bl->ke = tile_n != ta::kTileN ? ta::kernel_g16_t8_wave(lanes, mode) : ta::lookup_kernel(grid, lanes, mode, trace, 2);
     const ta::KernelEntry& ke = bl->ke;
     if (!ke.fn) return fail(TA_ERR_LOGIC, "no wave kernel instantiation for grid " + std::to_string(grid));
     TA_CK(cudaFuncSetAttribute(ke.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ke.smem)));
@@ -886,7 +911,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
     if (per_sm < 1) return fail(TA_ERR_CUDA, "wavefront kernel does not fit on an SM");
     WavePlan plan;
     int ctas = 0;
-    plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, grid, int64_t(bt->a.size()), &plan, &ctas);
+    plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, grid, int64_t(bt->a.size()), &plan, &ctas, tile_n);
     bl->ctas = ctas;
     bl->rounds = plan.rounds;
     TA_CK(bl->items.reserve(plan.items.size()));
@@ -902,7 +927,7 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
     TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
     TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
-    bl->padded = plan.padded_slices * grid * grid * ta::kTileN * ta::kTileN;
+    bl->padded = plan.padded_slices * grid * grid * tile_n * tile_n;
     return TA_OK;
   }
   bool multi = false;
@@ -1455,7 +1480,7 @@ int run_impl(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cudaS
           bt->plan_cache.push_back(std::make_unique<BucketLaunch>());
           if (int rc = prepare_bucket(bt, part, ta::kGridSizes[gi], w == 2 ? lanes8 : lanes_of[size_t(gi)], opt.mode,
                                       false, st, bt->plan_cache.back().get(), w == 1,
-                                      w == 2 ? ta::kSmallTileN : ta::kTileN))
+                                      w == 2 ? ta::kSmallTileN : w == 1 ? wave_tile_n() : ta::kTileN))
             return rc;
         }
       }
@@ -1932,7 +1957,7 @@ int align_scores_pipelined(DeviceCtx* ctx, const char* seqs, const int64_t* offs
         if (part.empty()) continue;
         BucketLaunch* bl = take_plan();
         rc = prepare_bucket(&shim, part, ta::kGridSizes[gi], w == 2 ? lanes8 : lanes, opt.mode, false, ctx->copy, bl,
-                            w == 1, w == 2 ? ta::kSmallTileN : ta::kTileN);
+                            w == 1, w == 2 ? ta::kSmallTileN : w == 1 ? wave_tile_n() : ta::kTileN);
         launch_now.push_back(bl);
       }
     }

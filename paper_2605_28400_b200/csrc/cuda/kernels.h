@@ -37,6 +37,10 @@ KernelEntry kernel_g16_wave_trace(int lanes, int mode);
 // 16 x 16 grid of 8 x 8 tiles, multi-block items only (blk 1, no trace): long
 // triplets whose extents pad less in 128-wide blocks than in 160-wide ones
 KernelEntry kernel_g16_t8(int lanes, int mode);
+// the same 8 x 8 tiles in wave mode (few long triplets, score only): a wave
+// step is latency bound per thread, so 64 instead of 100 cells per tile-step
+// shortens every step of the triplet's critical path
+KernelEntry kernel_g16_t8_wave(int lanes, int mode);
 
 inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int blk) {
   if (blk == 2) return grid != 16 ? KernelEntry{} : trace ? kernel_g16_wave_trace(lanes, mode) : kernel_g16_wave(lanes, mode);
@@ -138,4 +142,25 @@ inline KernelEntry lookup_kernel(int grid, int lanes, int mode, bool trace, int 
     }                                                                                  \
     return {};                                                                         \
   }                                                                                    \
+  }
+
+#define TA_DEFINE_T8_WAVE_TABLE()                                                                  \
+  namespace ta {                                                                                   \
+  KernelEntry kernel_g16_t8_wave(int lanes, int mode) {                                            \
+    constexpr int N8 = kSmallTileN;                                                                \
+    if (lanes == 1) {                                                                              \
+      switch (mode) {                                                                              \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 1, kGlobal, false, 2>, WaveSmem<N8, 16, 1, 2>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 1, kSemi, false, 2>, WaveSmem<N8, 16, 1, 2>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 1, kLocal, false, 2>, WaveSmem<N8, 16, 1, 2>::bytes, 256, 16};   \
+      }                                                                                            \
+    } else {                                                                                       \
+      switch (mode) {                                                                              \
+        case kGlobal: return {&wavefront_kernel<N8, 16, 2, kGlobal, false, 2>, WaveSmem<N8, 16, 2, 2>::bytes, 256, 16}; \
+        case kSemi: return {&wavefront_kernel<N8, 16, 2, kSemi, false, 2>, WaveSmem<N8, 16, 2, 2>::bytes, 256, 16};     \
+        case kLocal: return {&wavefront_kernel<N8, 16, 2, kLocal, false, 2>, WaveSmem<N8, 16, 2, 2>::bytes, 256, 16};   \
+      }                                                                                            \
+    }                                                                                              \
+    return {};                                                                                     \
+  }                                                                                                \
   }
