@@ -869,6 +869,19 @@ void split_largest(const std::vector<int32_t>& bucket, const std::vector<int32_t
   *lanes8 = s16_ok(scheme, bound8) ? 2 : 1;
 }
 
+// Wave launches of `ids` with tile side n: one block pair per resident CTA and
+// round, rounds run one after another (plan_wave); smaller tiles make more
+// blocks, so they pay only while they need no more rounds.
+int64_t wave_rounds(const ta_batch* bt, const std::vector<int32_t>& ids, int grid, int n, int lanes) {
+  int64_t blocks = 0;
+  for (int32_t id : ids) {
+    const Blocks bl = blocks_of(bt->b[size_t(id)], bt->c[size_t(id)], grid, n);
+    blocks += int64_t(bl.bj) * bl.bk;
+  }
+  const int64_t per_round = int64_t(std::max(1, bt->ctx->sms)) * lanes;
+  return (blocks + per_round - 1) / per_round;
+}
+
 // Tile side of score-only wave buckets: a wave step is latency bound per
 // thread, so the 8 x 8 tiles (64 cells per tile-step instead of 100) shorten
 // every step of a long triplet's critical path.  TA_WAVE_TILE=10 selects the
@@ -900,6 +913,8 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
       };
       if (ext(tile_n) > ext(ta::kTileN)) tile_n = ta::kTileN;
     }
+    if (tile_n != ta::kTileN && wave_rounds(bt, ids, grid, tile_n, lanes) > wave_rounds(bt, ids, grid, ta::kTileN, lanes))
+      tile_n = ta::kTileN;
     if (tile_n != ta::kTileN && (grid != 16 || trace))
       return fail(TA_ERR_LOGIC, "8 x 8-tile wave kernels exist for score items of grid 16 only");
     bl->ke = tile_n != ta::kTileN ? ta::kernel_g16_t8_wave(lanes, mode) : ta::lookup_kernel(grid, lanes, mode, trace, 2);
@@ -1072,11 +1087,37 @@ bool prefer_aff4(int32_t b, int32_t c) {
   return double(b4.bj * b4.bk) * g4 * g4 * ratio < double(b5.bj * b5.bk) * g5 * g5;
 }
 
+// Tile side of affine score-only wave buckets (see wave_tile_n): 4 x 4 tiles,
+// TA_AFF_WAVE_TILE=5 selects the 5 x 5 kernels (dev-only A/B knob).
+int aff_wave_tile_n() {
+  static const int n = [] {
+    const char* e = std::getenv("TA_AFF_WAVE_TILE");
+    return e && std::atoi(e) == ta::kAffN ? ta::kAffN : ta::kAffSmallN;
+  }();
+  return n;
+}
+
 int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mode, bool trace, int blk,
                 cudaStream_t st, BucketLaunch* bl, ta::AffEntry* ae, int tile_n = ta::kAffN) {
-  if (tile_n != ta::kAffN && (blk != 1 || trace))
-    return fail(TA_ERR_LOGIC, "4 x 4 affine tiles exist for block score items only");
-  *ae = tile_n != ta::kAffN ? ta::affine_kernel_blocks4(lanes, mode) : ta::lookup_affine(lanes, mode, trace, blk);
+  if (blk == 2) {
+    // the lane width was proven for 80-wide blocks: keep 4 x 4 tiles only while
+    // no triplet's 64-padded extents exceed its 80-padded ones (aff_lane_bound)
+    for (int32_t id : ids) {
+      if (tile_n == ta::kAffN) break;
+      auto ext = [&](int n) {
+        const int64_t gn = int64_t(ta::kAffG) * n;
+        return ((bt->b[size_t(id)] + gn) / gn + (bt->c[size_t(id)] + gn) / gn) * gn;
+      };
+      if (ext(tile_n) > ext(ta::kAffN)) tile_n = ta::kAffN;
+    }
+    if (tile_n != ta::kAffN && wave_rounds(bt, ids, ta::kAffG, tile_n, lanes) > wave_rounds(bt, ids, ta::kAffG, ta::kAffN, lanes))
+      tile_n = ta::kAffN;
+  }
+  if (tile_n != ta::kAffN && (blk == 0 || trace))
+    return fail(TA_ERR_LOGIC, "4 x 4 affine tiles exist for block / wave score items only");
+  *ae = tile_n == ta::kAffN ? ta::lookup_affine(lanes, mode, trace, blk)
+        : blk == 2          ? ta::affine_kernel_wave4(lanes, mode)
+                            : ta::affine_kernel_blocks4(lanes, mode);
   if (!ae->fn) return fail(TA_ERR_LOGIC, "no affine kernel instantiation");
   TA_CK(cudaFuncSetAttribute(ae->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(ae->smem)));
   int per_sm = 0;
@@ -1088,7 +1129,7 @@ int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mo
     WavePlan plan;
     int ctas = 0;
     plan_wave(ids, bt->a, bt->b, bt->c, per_sm * bt->ctx->sms, lanes, ta::kAffG, int64_t(bt->a.size()), &plan, &ctas,
-              ta::kAffN, true);
+              tile_n, true);
     bl->grid = ta::kAffG;
     bl->lanes = lanes;
     bl->mode = mode;
@@ -1107,7 +1148,7 @@ int aff_prepare(ta_batch* bt, const std::vector<int32_t>& ids, int lanes, int mo
     TA_CK(cudaMemcpyAsync(bl->items.ptr, plan.items.data(), plan.items.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
     TA_CK(cudaMemcpyAsync(bl->soff.ptr, plan.soff.data(), plan.soff.size() * 4, cudaMemcpyHostToDevice, st));
     TA_CK(cudaMemcpyAsync(bl->steps.ptr, plan.steps.data(), plan.steps.size() * 4, cudaMemcpyHostToDevice, st));
-    bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * ta::kAffN * ta::kAffN;
+    bl->padded = plan.padded_slices * ta::kAffG * ta::kAffG * tile_n * tile_n;
     return TA_OK;
   }
   const int64_t want = (int64_t(ids.size()) + lanes - 1) / lanes;
@@ -1252,7 +1293,7 @@ int run_affine(ta_batch* bt, const ta_scheme& scheme, const ta_options& opt, cud
         bt->aff_cache.emplace_back();
         if (int rc = aff_prepare(bt, part, w == 3 ? lanes4 : lanes, opt.mode, false, w == 3 ? 1 : w, st,
                                  bt->plan_cache.back().get(), &bt->aff_cache.back(),
-                                 w == 3 ? ta::kAffSmallN : ta::kAffN))
+                                 w == 3 ? ta::kAffSmallN : w == 2 ? aff_wave_tile_n() : ta::kAffN))
           return rc;
       }
       bt->plan_key = key;

@@ -28,6 +28,9 @@ AffEntry affine_kernel_wave(int lanes, int mode, bool trace);
 // 4 x 4 tiles, block items only (no trace): long triplets whose extents pad
 // less in 64-wide blocks than in 80-wide ones
 AffEntry affine_kernel_blocks4(int lanes, int mode);
+// the same 4 x 4 tiles in wave mode (few long triplets, score only): 16
+// instead of 25 cells per latency-bound wave step
+AffEntry affine_kernel_wave4(int lanes, int mode);
 
 inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
   if (blk == 2) return affine_kernel_wave(lanes, mode, trace);
@@ -89,4 +92,27 @@ inline AffEntry lookup_affine(int lanes, int mode, bool trace, int blk) {
     }                                                   \
     return {};                                          \
   }                                                     \
+  }
+
+#define TA_AFF4W_ENTRY(L, M) \
+  AffEntry{&affine_kernel<kAffSmallN, kAffG, L, M, false, 2>, AffSmem<kAffSmallN, kAffG, L, 2>::bytes, kAffG * kAffG}
+
+#define TA_DEFINE_AFF4W_TABLE()                          \
+  namespace ta {                                         \
+  AffEntry affine_kernel_wave4(int lanes, int mode) {    \
+    if (lanes == 1) {                                    \
+      switch (mode) {                                    \
+        case kGlobal: return TA_AFF4W_ENTRY(1, kGlobal); \
+        case kSemi: return TA_AFF4W_ENTRY(1, kSemi);     \
+        case kLocal: return TA_AFF4W_ENTRY(1, kLocal);   \
+      }                                                  \
+    } else {                                             \
+      switch (mode) {                                    \
+        case kGlobal: return TA_AFF4W_ENTRY(2, kGlobal); \
+        case kSemi: return TA_AFF4W_ENTRY(2, kSemi);     \
+        case kLocal: return TA_AFF4W_ENTRY(2, kLocal);   \
+      }                                                  \
+    }                                                    \
+    return {};                                           \
+  }                                                      \
   }
