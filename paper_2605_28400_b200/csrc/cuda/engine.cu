@@ -754,9 +754,17 @@ void plan_wave(const std::vector<int32_t>& ids, const std::vector<int32_t>& a, c
     return make_int4(x.id, (x.J << 16) | x.K, a[size_t(x.id)] + 1, (bl.bj << 16) | bl.bk);
   };
   std::vector<std::pair<int4, int4>> pairs;  // (lane 0, lane 1); lane 1 may be a null item
+  // Pairing halves the CTAs but doubles every face CTA's per-step face work
+  // (the step is latency bound on the face warp): pair only when the blocks
+  // outnumber the resident CTAs (TA_WAVE_PAIR=1 forces pairing: dev A/B knob).
+  static const bool force_pair = [] {
+    const char* e = std::getenv("TA_WAVE_PAIR");
+    return e && std::atoi(e) == 1;
+  }();
+  const bool pair = force_pair || blks.size() > size_t(std::max(1, max_ctas));
   for (size_t i = 0; i < blks.size();) {
     const int4 x = rec(blks[i]);
-    if (lanes == 2 && i + 1 < blks.size()) {
+    if (lanes == 2 && pair && i + 1 < blks.size()) {
       const Blk& u = blks[i];
       const Blk& v = blks[i + 1];
       const bool independent = u.id != v.id || u.d == v.d;
