@@ -923,6 +923,13 @@ int prepare_bucket(ta_batch* bt, const std::vector<int32_t>& ids, int grid, int 
     }
     if (tile_n != ta::kTileN && wave_rounds(bt, ids, grid, tile_n, lanes) > wave_rounds(bt, ids, grid, ta::kTileN, lanes))
       tile_n = ta::kTileN;
+    // blocks that fit one per resident CTA run unpaired (plan_wave): the
+    // int32-lane kernel then carries no idle partner lane
+    static const bool lanes1 = [] {
+      const char* e = std::getenv("TA_WAVE_LANES1");
+      return !(e && std::atoi(e) == 0);
+    }();
+    if (lanes1 && lanes == 2 && wave_rounds(bt, ids, grid, tile_n, 1) <= 1) bl->lanes = lanes = 1;
     if (tile_n != ta::kTileN && (grid != 16 || trace))
       return fail(TA_ERR_LOGIC, "8 x 8-tile wave kernels exist for score items of grid 16 only");
     bl->ke = tile_n != ta::kTileN ? ta::kernel_g16_t8_wave(lanes, mode) : ta::lookup_kernel(grid, lanes, mode, trace, 2);
